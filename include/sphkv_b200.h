@@ -1,0 +1,253 @@
+/*
+ * sphkv_b200.h -- C ABI of the B200-native Spherical-KV decode hot path.
+ *
+ * One shared library, libsphkv_b200.so, built for sm_100a only.  Every entry
+ * point is `extern "C"`, takes plain pointers / sizes / a cudaStream_t, and
+ * returns an int status (0 == SPHKV_OK).  All data buffers are caller-owned
+ * DEVICE pointers unless the parameter name ends in `_host`.  The library
+ * keeps no global mutable state; `sphkv_last_error()` is thread-local.
+ *
+ * The reference (arXiv 2605.18856, read-only `sphkv` Python package, paths
+ * below relative to pkg/src/sphkv/) has no FFI: its boundary is the Python
+ * API exported from __init__.py:4-18.  Each entry point cites the reference
+ * function it replaces; INTEGRATION.md shows the ctypes binding a maintainer
+ * would add on the reference side.
+ *
+ * Device page format:
+ *   code pool  : per page a 16-byte aligned block = (d-1) angle rows of
+ *                page_size*angle_bits bits (coordinate-major, LSB-first, the
+ *                reference SoA stream of store.py:205-208 with stride
+ *                page_size) followed by one radius row of page_size*radius_bits
+ *                bits, padded to 16 bytes.  For a full page the angle rows are
+ *                byte-identical to Page.angle_stream(); partial pages are
+ *                re-strided by sphkv_export_streams().
+ *   value pool : fp16 [page][page_size][d_v]; inside each row the 16-byte
+ *                chunk c of item i is stored at chunk (c ^ (i & 7)) so that
+ *                1-D bulk copies land ldmatrix-conflict-free in shared memory.
+ */
+#ifndef SPHKV_B200_H
+#define SPHKV_B200_H
+
+#include <stdint.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPHKV_ABI_VERSION 1
+
+enum {
+  SPHKV_OK = 0,
+  SPHKV_E_VALUE = 1,        /* -> ValueError   (bad argument / range)          */
+  SPHKV_E_KEY = 2,          /* -> KeyError     (unknown head / missing state)  */
+  SPHKV_E_INFEASIBLE = 3,   /* -> InfeasibleProtectionError (controller.py:46) */
+  SPHKV_E_UNSUPPORTED = 4,  /* -> ValueError   (outside the kernel contract)   */
+  SPHKV_E_CUDA = 5,         /* -> RuntimeError (CUDA error)                    */
+  SPHKV_E_CAPACITY = 6      /* -> RuntimeError (store pool exhausted)          */
+};
+
+enum { SPHKV_F32 = 0, SPHKV_F64 = 1, SPHKV_BF16 = 2, SPHKV_F16 = 3 };
+
+#define SPHKV_MAX_TIERS 16
+
+/* One precision tier (codec.py:73-107 TierSpec + TierTable eps constants). */
+typedef struct {
+  int32_t id;
+  int32_t angle_bits;
+  int32_t radius_bits;
+  int32_t meta_bits;
+  double eps_theta;
+  double eps_r;
+} sphkv_tier_t;
+
+/* Device page descriptor, 32 bytes (the reference Page, store.py:136-211). */
+typedef struct {
+  uint64_t code_off;     /* byte offset of the page's code block             */
+  double radius_scale;   /* page radius scale (fp64, store.py:465 / :264)   */
+  float rscale;          /* (float)(radius_scale / (2^radius_bits - 1))      */
+  int32_t count;         /* items stored                                     */
+  int32_t group;         /* (seq*layers + layer)*heads + head                */
+  uint8_t tier;          /* tier id                                          */
+  uint8_t abits;
+  uint8_t rbits;
+  uint8_t mbits;
+} sphkv_page_t;
+
+/* Paged store: pools and tables (PagedStore, store.py:214-427). */
+typedef struct {
+  int32_t batch, layers, heads, d, d_v, page_size;
+  int32_t n_tiers;            /* entries in `tiers`, drop tier first          */
+  int32_t max_pages;          /* capacity of the page-indexed pools          */
+  int32_t ptr_cap;            /* pointer-list capacity per group             */
+  int32_t _pad;
+  uint64_t code_cap;          /* bytes in `codes`                             */
+  sphkv_tier_t tiers[SPHKV_MAX_TIERS];
+  sphkv_page_t* pages;        /* [max_pages]                                  */
+  int32_t* ptr;               /* [groups * ptr_cap] page ids, pointer order   */
+  int32_t* ptr_len;           /* [groups]                                     */
+  int32_t* group_last;        /* [groups * SPHKV_MAX_TIERS] last page / -1    */
+  uint8_t* codes;             /* code pool                                    */
+  uint16_t* values;           /* fp16 value pool [max_pages][P][d_v]          */
+  uint8_t* protect;           /* [max_pages][P]                               */
+  int64_t* token_ids;         /* [max_pages][P]                               */
+  uint64_t* counters;         /* [0]=n_pages [1]=code bytes used (device)     */
+} sphkv_store_t;
+
+/* Dense bf16-K / fp16-V paged store used by the dense baseline kernel
+ * (DenseStore, store.py:485-569). K pages are [P][d] bf16, swizzled like V. */
+typedef struct {
+  int32_t batch, layers, heads, d, d_v, page_size;
+  int32_t n_pages_per_group;  /* ceil(T / P)                                  */
+  int32_t tokens;             /* T (items per group)                          */
+  uint16_t* keys;             /* bf16 [groups][n_pages][P][d]                 */
+  uint16_t* values;           /* fp16 [groups][n_pages][P][d_v]               */
+} sphkv_dense_store_t;
+
+/* One decode work unit: a contiguous range of one group's pointer list. */
+typedef struct {
+  int32_t group;              /* (seq*layers + layer)*heads + head            */
+  int32_t ptr_begin;          /* first pointer-list position                  */
+  int32_t ptr_end;            /* one past the last                            */
+  int32_t out_slot;           /* index into the partial buffer                */
+} sphkv_unit_t;
+
+/* Controller features (ControllerFeatures, controller.py:77-96). */
+typedef struct {
+  const double* u_hat;        /* [layers*heads] (per sequence if batched: [B*L*H]) */
+  const double* s_hat;        /* same shape as u_hat                          */
+  const double* omega_tok;    /* [tokens] omega of each prefill token         */
+  double r_q;
+  double alpha_theta;
+  double alpha_r;
+  double omega_recent;        /* omega of decode-appended states (:96)         */
+} sphkv_features_t;
+
+int sphkv_abi_version(void);
+const char* sphkv_last_error(void);
+int sphkv_device_ok(void);
+
+/* ---- encode (codec.py:222-257, decode.py:457-459) ------------------------ */
+
+/* radii[n] = || keys[n, :] || in fp64 with numpy's pairwise summation order. */
+int sphkv_encode_radii(const void* keys, int dtype, int64_t n, int d,
+                       double* radii, cudaStream_t stream);
+
+/* to_spherical / angles_from_unit, batched: radii[n] and angles[n, d-1]. */
+int sphkv_encode(const void* keys, int dtype, int64_t n, int d,
+                 double* radii, double* angles, cudaStream_t stream);
+
+/* angles_from_unit (codec.py:239-257) on rows that are already unit length. */
+int sphkv_angles_from_unit(const double* u, int64_t n, int d, double* angles,
+                           cudaStream_t stream);
+
+/* quantize_angles (codec.py:326-340): codes[n, d-1] (uint32) at `bits`. */
+int sphkv_quantize_angles(const double* angles, int64_t n, int dm1, int bits,
+                          uint32_t* codes, cudaStream_t stream);
+
+/* ---- RDR controller (controller.py:201-386) ----------------------------- */
+
+/* score_states: best_tier int16, score/nu/d_drop fp64 over [n = L*H*T]
+ * states.  `seg_omega` is omega per token (length T), u_hat/s_hat per
+ * (l, h) [L*H].  Bit-exact with numpy's fp64 operation order. */
+int sphkv_rdr_score(const double* radii, const double* u_hat, const double* s_hat,
+                    const double* seg_omega, double r_q, double alpha_theta,
+                    double alpha_r, const sphkv_tier_t* tiers_host, int n_tiers,
+                    double lam, const uint8_t* protect, int layers, int heads,
+                    int tokens, int d, int16_t* best_tier, double* score,
+                    double* nu, double* d_drop, cudaStream_t stream);
+
+/* Scratch bytes for allocate_greedy / downtier over n states. */
+int64_t sphkv_rdr_workspace_bytes(int64_t n);
+
+/* allocate_greedy: z int8 / tier int16 outputs.  Exact parallel form: stable
+ * radix sort on (-nu, flat index) then <= (#distinct rates) filtered scans.
+ * Returns SPHKV_E_INFEASIBLE when protected demand exceeds the budget. */
+int sphkv_rdr_allocate_greedy(const int16_t* best_tier, const double* nu,
+                              const uint8_t* protect, int64_t n,
+                              const sphkv_tier_t* tiers_host, int n_tiers, int d,
+                              int64_t budget_bits, void* workspace, int8_t* z,
+                              int16_t* tier, cudaStream_t stream);
+
+/* downtier_before_drop from the full best-tier start (controller.py:349-398). */
+int sphkv_rdr_downtier(const int16_t* best_tier, const double* nu,
+                       const uint8_t* protect, int64_t n,
+                       const sphkv_tier_t* tiers_host, int n_tiers, int d,
+                       int64_t budget_bits, void* workspace, int8_t* z,
+                       int16_t* tier, cudaStream_t stream);
+
+/* ---- paged store (store.py:214-482) ------------------------------------- */
+
+/* Reset counters / pointer lists of a store (pools are zeroed by caller). */
+int sphkv_store_reset(const sphkv_store_t* st, cudaStream_t stream);
+
+/* pack_pages_arrays fused with the encoder: dense keys [B*L*H*T, d] (fp32 /
+ * bf16 / fp64), fp16 values, assignment (z int8, tier int16, protect u8)
+ * and fp64 radii -> pages in pointer order (l, h) -> tier -> chunk.
+ * `angles` may be NULL (encode from keys) or fp64 [.., d-1] (drop-in path
+ * with caller-supplied angles, as pack_pages_arrays takes them). */
+int sphkv_pack_pages(const sphkv_store_t* st, const void* keys, int key_dtype,
+                     const double* angles, const double* radii,
+                     const uint16_t* values, const int8_t* z, const int16_t* tier,
+                     const uint8_t* protect, int tokens, void* workspace,
+                     int64_t workspace_bytes, cudaStream_t stream);
+int64_t sphkv_pack_workspace_bytes(int batch, int layers, int heads, int tokens);
+
+/* PagedStore.append_item for one new state per group (decode.py:454-498):
+ * keys [groups, d] (fp64 radius/angles computed on device unless `angles`
+ * given), values fp16 [groups, d_v], tier_ids int16 [groups] (0 = drop),
+ * protect u8 [groups], token id per group.  Pages open in group order. */
+int sphkv_append(const sphkv_store_t* st, const void* keys, int key_dtype,
+                 const double* radii, const double* angles, const uint16_t* values,
+                 const int16_t* tier_ids, const uint8_t* protect,
+                 const int64_t* token_ids, const uint8_t* active, void* workspace,
+                 cudaStream_t stream);
+int64_t sphkv_append_workspace_bytes(int groups);
+
+/* score_and_best_tier for appended states (controller.py:181-198). */
+int sphkv_score_append(const double* radii, int groups_per_seq, int heads,
+                       const double* u_hat, const double* s_hat, double r_q,
+                       double omega, double alpha_theta, double alpha_r,
+                       const sphkv_tier_t* tiers_host, int n_tiers, double lam,
+                       int d, int64_t n, int16_t* tier_out, double* score_out,
+                       double* nu_out, cudaStream_t stream);
+
+/* Dense baseline store fill (DenseStore.bulk_load, store.py:524-531): keys
+ * [groups*T, d] (dtype), values fp16 [groups*T, d_v] -> swizzled pages. */
+int sphkv_dense_fill(const sphkv_dense_store_t* st, const void* keys, int key_dtype,
+                     const uint16_t* values, cudaStream_t stream);
+
+/* Reference-format streams of every page: angle stream (stride = count),
+ * radius stream, fp16 values un-swizzled [count][d_v], protect bytes.
+ * offsets_host give each page's byte offset in `out`. */
+int sphkv_export_streams(const sphkv_store_t* st, int n_pages,
+                         const int64_t* offsets, uint8_t* out, cudaStream_t stream);
+
+/* ---- decode (decode.py:291-355) ------------------------------------------ */
+
+/* ADA paged decode: q fp32 [B, L, H*G, d]; per unit writes the partial
+ * softmax state (m[G], l[G], acc[G][d_v]) in base-2 logit units to
+ * partials[out_slot].  logits_dbg (optional, fp32) receives logits (natural
+ * units) at [unit item index] for parity checks; pass NULL in production. */
+int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
+                     const sphkv_unit_t* units, int n_units, float* partials,
+                     float* logits_dbg, const int64_t* dbg_offsets, int grid,
+                     cudaStream_t stream);
+
+/* Dense bf16 paged decode with the same unit/partial contract. */
+int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,
+                       const sphkv_unit_t* units, int n_units, float* partials,
+                       int grid, cudaStream_t stream);
+
+/* Split-context LSE merge: out fp32 [n_groups*G, d_v]; group g's partials
+ * are slots [slot_begin[g], slot_begin[g+1]). Empty splits carry m = -inf. */
+int sphkv_lse_merge(const float* partials, const int32_t* slot_begin,
+                    int n_groups, int G, int d_v, float* out, cudaStream_t stream);
+
+/* Bytes per partial slot for G query heads and d_v. */
+int64_t sphkv_partial_floats(int G, int d_v);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPHKV_B200_H */

@@ -1,0 +1,853 @@
+// ADA paged decode, dense bf16 paged decode and the split-context LSE merge.
+//
+// Reference behaviour replaced (pkg/src/sphkv/):
+//   decode.py:123-192  angle-path logits  l = (r_q/sqrt d) * r~ * (feat . qfeat)
+//   decode.py:291-355  _head_attend: pointer-order stream, stable softmax,
+//                      blockwise value mix
+//   decode.py:63-69, 302-307  dense path (DenseStore)
+//   decode.py:347-354  one softmax over all logits  ->  split partials + LSE
+//
+// ADA kernel (one persistent CTA per SM, ~210 KB smem):
+//   warps 0..NL-1  logit warps: a 128-item tile per warp, 4 items per lane.
+//                  Angle codes are read straight from the page's coordinate-
+//                  major rows (L2-prefetched by cp.async.bulk.prefetch),
+//                  (cos, sin) of polar codes come from a shared-memory LUT,
+//                  the feature recurrence runs in fp32 registers and the G
+//                  query heads are dotted with packed FFMA2.  Tile max/sum
+//                  and fp16 weights go to a P slot.
+//   warp NL        PV warp: V^T (ldmatrix.trans of the TMA-staged, swizzled
+//                  fp16 V tile) x P (fp16) on mma.sync, fp32 accumulate,
+//                  online-softmax combine across tiles, writes the partial.
+//   warp NL+1      producer: 1-D TMA bulk copies of V tiles into a ring.
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace sphkv {
+
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr int ADA_NL = 8;          // logit warps
+constexpr int ADA_TI = 128;        // items per tile (4 per lane)
+constexpr int ADA_NS = 16;         // P slots
+constexpr int ADA_NV = 4;          // V slots
+constexpr int ADA_THREADS = (ADA_NL + 2) * 32;
+constexpr int MAX_UNIT_TILES = 1024;
+constexpr int LUT_MAX_BITS = 12;
+constexpr int LUT_BUDGET = 6144;   // float2 entries (48 KB)
+constexpr int PROW_PAD = 16;       // bytes of padding per P row (bank spread)
+
+struct AdaParams {
+  sphkv_store_t st;
+  const float* q;          // [groups, G, d] fp32
+  int G;
+  const sphkv_unit_t* units;
+  int n_units;
+  float* partials;
+  float* logits_dbg;
+  const int64_t* dbg_off;
+  int lut_off[SPHKV_MAX_TIERS];   // float2 offset of each tier's polar LUT, -1 = none
+  int lut_entries;
+  int TI;                   // tile items (min(P, 128))
+  int dvp;                  // d_v padded to 16
+  uint32_t smem_q, smem_tiles, smem_p, smem_v, smem_bar;  // byte offsets
+  int pslot_bytes, prow_bytes;
+};
+
+__device__ __forceinline__ int tier_index(const sphkv_store_t& st, int tier_id) {
+  for (int i = 0; i < st.n_tiers; ++i)
+    if (st.tiers[i].id == tier_id) return i;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// logit tile: 4 consecutive items per lane, G heads (GP packed pairs)
+// ---------------------------------------------------------------------------
+template <int B>
+struct CodeWin {
+  static constexpr int MAXSH = (B % 2) ? 28 : ((B % 4) ? 24 : ((B % 8) ? 16 : 0));
+  static constexpr int WORDS = (4 * B <= 32 && MAXSH + 4 * B <= 32) ? 1
+                             : (MAXSH + 4 * B <= 64 ? 2 : 3);
+};
+
+template <int B>
+__device__ __forceinline__ void extract4(const uint32_t* __restrict__ row, int w, int sh,
+                                         uint32_t c[4]) {
+  constexpr uint32_t M = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
+  if constexpr (CodeWin<B>::WORDS == 1) {
+    uint32_t x = __ldg(row + w) >> sh;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = (x >> (k * B)) & M;
+  } else if constexpr (CodeWin<B>::WORDS == 2) {
+    uint32_t lo = __ldg(row + w), hi = __ldg(row + w + 1);
+    uint32_t a = __funnelshift_r(lo, hi, sh);
+    uint32_t b = sh ? (hi >> sh) : hi;
+    uint64_t y = ((uint64_t)b << 32) | a;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = (uint32_t)(y >> (k * B)) & M;
+  } else {
+    uint32_t w0 = __ldg(row + w), w1 = __ldg(row + w + 1), w2 = __ldg(row + w + 2);
+    uint32_t a = __funnelshift_r(w0, w1, sh);
+    uint32_t b = __funnelshift_r(w1, w2, sh);
+    uint64_t y = ((uint64_t)b << 32) | a;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c[k] = (uint32_t)(y >> (k * B)) & M;
+  }
+}
+
+__device__ __forceinline__ uint32_t read_bits_g(const uint32_t* __restrict__ words, uint64_t bit,
+                                                int nbits) {
+  uint64_t w = bit >> 5;
+  int sh = (int)(bit & 31);
+  uint32_t lo = __ldg(words + w);
+  uint32_t hi = (sh + nbits > 32) ? __ldg(words + w + 1) : 0u;
+  uint32_t v = __funnelshift_r(lo, hi, sh);
+  return nbits >= 32 ? v : (v & ((1u << nbits) - 1u));
+}
+
+template <int B, int GP>
+__device__ __forceinline__ void ada_logit_tile(const AdaParams& p, const sphkv_page_t& pg, int sub,
+                                            int lane, const float2* __restrict__ qs,
+                                            const float2* __restrict__ lut,
+                                            float lg[4][2 * GP]) {
+  const sphkv_store_t& st = p.st;
+  const int d = st.d, P = st.page_size;
+  const int item0 = sub * p.TI + 4 * lane;
+  const uint32_t* base = reinterpret_cast<const uint32_t*>(st.codes + pg.code_off);
+  const int row_words = P * B / 32;
+  const uint32_t obit = (uint32_t)item0 * B;
+  const int w = (int)(obit >> 5), sh = (int)(obit & 31);
+
+  float prod[4];
+  ptx::f2 acc[4][GP];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    prod[k] = 1.0f;
+#pragma unroll
+    for (int g = 0; g < GP; ++g) acc[k][g] = ptx::f2_make(0.f, 0.f);
+  }
+  const float pstep = (float)(1.0 / (double)((1u << B) - 1u));
+
+#pragma unroll 4
+  for (int j = 0; j < d - 2; ++j) {
+    uint32_t c[4];
+    extract4<B>(base + (size_t)j * row_words, w, sh, c);
+    ptx::f2 qv[GP];
+#pragma unroll
+    for (int g = 0; g < GP; ++g) qv[g].v = *reinterpret_cast<const unsigned long long*>(&qs[j * GP + g]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float cs, sn;
+      if (B <= LUT_MAX_BITS && lut != nullptr) {
+        float2 t = lut[c[k]];
+        cs = t.x;
+        sn = t.y;
+      } else {
+        sincospif((float)c[k] * pstep, &sn, &cs);
+      }
+      float f = prod[k] * cs;
+#pragma unroll
+      for (int g = 0; g < GP; ++g) acc[k][g] = ptx::f2_fma_s(f, qv[g], acc[k][g]);
+      prod[k] *= sn;
+    }
+  }
+  // circular last angle (row d-2): step 2*pi/2^B  ->  sincospi(code * 2^(1-B))
+  {
+    uint32_t c[4];
+    extract4<B>(base + (size_t)(d - 2) * row_words, w, sh, c);
+    ptx::f2 qa[GP], qb[GP];
+#pragma unroll
+    for (int g = 0; g < GP; ++g) {
+      qa[g].v = *reinterpret_cast<const unsigned long long*>(&qs[(d - 2) * GP + g]);
+      qb[g].v = *reinterpret_cast<const unsigned long long*>(&qs[(d - 1) * GP + g]);
+    }
+    const float cstep = ldexpf(1.0f, 1 - B);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float sn, cs;
+      sincospif((float)c[k] * cstep, &sn, &cs);
+      float f0 = prod[k] * cs, f1 = prod[k] * sn;
+#pragma unroll
+      for (int g = 0; g < GP; ++g) {
+        acc[k][g] = ptx::f2_fma_s(f0, qa[g], acc[k][g]);
+        acc[k][g] = ptx::f2_fma_s(f1, qb[g], acc[k][g]);
+      }
+    }
+  }
+  // radii (row d-1 holds the radius stream)
+  const uint64_t rbit0 = (uint64_t)(d - 1) * P * B;
+  const int rb = pg.rbits;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint32_t rc = read_bits_g(base, rbit0 + (uint64_t)(item0 + k) * rb, rb);
+    float rr = (float)rc * pg.rscale;
+#pragma unroll
+    for (int g = 0; g < GP; ++g) {
+      lg[k][2 * g] = rr * ptx::f2_lo(acc[k][g]);
+      lg[k][2 * g + 1] = rr * ptx::f2_hi(acc[k][g]);
+    }
+  }
+}
+
+template <int GP>
+__device__ void ada_logit_dispatch(int B, const AdaParams& p, const sphkv_page_t& pg, int sub,
+                                   int lane, const float2* qs, const float2* lut,
+                                   float lg[4][2 * GP]) {
+  switch (B) {
+#define SPHKV_CASE(b) \
+  case b: ada_logit_tile<b, GP>(p, pg, sub, lane, qs, lut, lg); break;
+    SPHKV_CASE(1) SPHKV_CASE(2) SPHKV_CASE(3) SPHKV_CASE(4) SPHKV_CASE(5) SPHKV_CASE(6)
+    SPHKV_CASE(7) SPHKV_CASE(8) SPHKV_CASE(9) SPHKV_CASE(10) SPHKV_CASE(11) SPHKV_CASE(12)
+    SPHKV_CASE(13) SPHKV_CASE(14) SPHKV_CASE(15) SPHKV_CASE(16)
+#undef SPHKV_CASE
+    default: break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// shared pieces: unit setup, P slot write, PV consumer
+// ---------------------------------------------------------------------------
+struct TileEntry {
+  int32_t page;       // page id
+  int32_t sub_off;    // (sub << 24) | item offset within unit (< 2^24)
+};
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Build the unit's tile list (warp 0): returns tile count (also in smem).
+__device__ int build_tiles(const sphkv_store_t& st, const sphkv_unit_t& u, int TI,
+                           TileEntry* tiles, int* ntiles_smem, int lane) {
+  const int* ptr = st.ptr + (size_t)u.group * st.ptr_cap;
+  int nt = 0, items = 0;
+  for (int b = u.ptr_begin; b < u.ptr_end; b += 32) {
+    int pos = b + lane;
+    int pid = -1, cnt = 0;
+    if (pos < u.ptr_end) {
+      pid = ptr[pos];
+      cnt = st.pages[pid].count;
+    }
+    int t = (cnt + TI - 1) / TI;
+    // inclusive scans of tiles and items
+    int ts = t, is = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int a = __shfl_up_sync(0xffffffffu, ts, o), c = __shfl_up_sync(0xffffffffu, is, o);
+      if (lane >= o) { ts += a; is += c; }
+    }
+    int t0 = nt + ts - t, i0 = items + is - cnt;
+    for (int s = 0; s < t; ++s) {
+      if (t0 + s < MAX_UNIT_TILES) {
+        tiles[t0 + s].page = pid;
+        tiles[t0 + s].sub_off = (s << 24) | (i0 + s * TI);
+      }
+    }
+    nt += __shfl_sync(0xffffffffu, ts, 31);
+    items += __shfl_sync(0xffffffffu, is, 31);
+  }
+  if (lane == 0) *ntiles_smem = nt < MAX_UNIT_TILES ? nt : MAX_UNIT_TILES;
+  return nt;
+}
+
+// Write the fp16 weights of one tile (4 items x G per lane) + tile max/sum.
+template <int NG>
+__device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int TI, int lane,
+                                            int G, const float lg[4][NG], int nvalid_lane) {
+  float* hdr = reinterpret_cast<float*>(slot + 8 * prow_bytes);
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < nvalid_lane) m = fmaxf(m, lg[k][g]);
+    m = warp_max(m);
+    float pv[4], s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float e = (k < nvalid_lane) ? exp2f(lg[k][g] - m) : 0.f;
+      __half h = __float2half_rn(e);
+      pv[k] = __half2float(h);
+      s += pv[k];
+    }
+    s = warp_sum(s);
+    if (g < G && 4 * lane < TI) {
+      uint2 packed;
+      packed.x = ptx::pack_half2(pv[0], pv[1]);
+      packed.y = ptx::pack_half2(pv[2], pv[3]);
+      *reinterpret_cast<uint2*>(slot + g * prow_bytes + (4 * lane) * 2) = packed;
+    }
+    if (lane == 0 && g < 8) {
+      hdr[g] = m;
+      hdr[8 + g] = s;
+    }
+  }
+}
+
+struct PVState {
+  float acc[8][4];
+  float m[2], l[2];
+};
+
+__device__ __forceinline__ void pv_init(PVState& s) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) s.acc[i][r] = 0.f;
+  s.m[0] = s.m[1] = -INFINITY;
+  s.l[0] = s.l[1] = 0.f;
+}
+
+// One tile of P.V on mma.sync + online combine.
+__device__ __forceinline__ void pv_tile(PVState& s, const uint8_t* pslot, const uint8_t* vslot,
+                                        int prow_bytes, int TI, int dvp, int MT, int G, int lane) {
+  float c[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c[i][r] = 0.f;
+  const int nchunks = dvp / 8;
+  const int smask = (nchunks < 8 ? nchunks : 8) - 1;
+  const uint32_t vbase = ptx::smem_u32(vslot);
+  const uint32_t pbase = ptx::smem_u32(pslot);
+  const int r = lane & 7, mat = lane >> 3;
+  for (int ks = 0; ks < TI / 16; ++ks) {
+    uint32_t b0, b1;
+    ptx::ldsm_x2(pbase + (lane & 7) * prow_bytes + (ks * 16 + ((lane >> 3) & 1) * 8) * 2, b0, b1);
+    const int item = ks * 16 + r + (mat >> 1) * 8;
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      if (mt < MT) {
+        int chunk = 2 * mt + (mat & 1);
+        int sw = chunk ^ (r & smask);
+        uint32_t a0, a1, a2, a3;
+        ptx::ldsm_x4_trans(vbase + (item * dvp + sw * 8) * 2, a0, a1, a2, a3);
+        ptx::mma_f16(c[mt], a0, a1, a2, a3, b0, b1);
+      }
+    }
+  }
+  const float* hdr = reinterpret_cast<const float*>(pslot + 8 * prow_bytes);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int g = 2 * (lane & 3) + h;
+    float mt_ = (g < G) ? hdr[g] : 0.f;
+    float lt = (g < G) ? hdr[8 + g] : 0.f;
+    float mn = fmaxf(s.m[h], mt_);
+    float al = exp2f(s.m[h] - mn), be = exp2f(mt_ - mn);
+    s.m[h] = mn;
+    s.l[h] = s.l[h] * al + lt * be;
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      s.acc[mt][h] = s.acc[mt][h] * al + c[mt][h] * be;
+      s.acc[mt][2 + h] = s.acc[mt][2 + h] * al + c[mt][2 + h] * be;
+    }
+  }
+}
+
+__device__ __forceinline__ void pv_write(const PVState& s, float* part, int G, int d_v, int MT,
+                                         int lane) {
+  // layout: m[G], l[G], acc[G][d_v]
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int g = 2 * (lane & 3) + h;
+    if (g >= G) continue;
+    if ((lane >> 2) == 0) {
+      part[g] = s.m[h];
+      part[G + g] = s.l[h];
+    }
+    float* a = part + 2 * G + (size_t)g * d_v;
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      if (mt >= MT) continue;
+      int r0 = mt * 16 + (lane >> 2);
+      if (r0 < d_v) a[r0] = s.acc[mt][h];
+      if (r0 + 8 < d_v) a[r0 + 8] = s.acc[mt][2 + h];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ADA kernel
+// ---------------------------------------------------------------------------
+template <int GP>
+__global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const sphkv_store_t& st = p.st;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2* lut = reinterpret_cast<float2*>(smem);
+  float2* qs = reinterpret_cast<float2*>(smem + p.smem_q);
+  TileEntry* tiles = reinterpret_cast<TileEntry*>(smem + p.smem_tiles);
+  int* ntiles_s = reinterpret_cast<int*>(smem + p.smem_tiles + MAX_UNIT_TILES * sizeof(TileEntry));
+  uint8_t* pslots = smem + p.smem_p;
+  uint8_t* vslots = smem + p.smem_v;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
+  uint64_t* p_full = bars;
+  uint64_t* p_empty = bars + ADA_NS;
+  uint64_t* v_full = bars + 2 * ADA_NS;
+  uint64_t* v_empty = bars + 2 * ADA_NS + ADA_NV;
+  const int d = st.d, P = st.page_size, TI = p.TI, dvp = p.dvp, MT = dvp / 16;
+  const uint32_t vbytes = (uint32_t)TI * dvp * 2;
+
+  // polar LUTs (fp64 sincos rounded to fp32), barrier init
+  for (int t = 0; t < st.n_tiers; ++t) {
+    int off = p.lut_off[t];
+    if (off < 0) continue;
+    int b = st.tiers[t].angle_bits;
+    int n = 1 << b;
+    double step = kPi / (double)((1u << b) - 1u);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      double sn, cs;
+      sincos((double)i * step, &sn, &cs);
+      lut[off + i] = make_float2((float)cs, (float)sn);
+    }
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ADA_NS; ++i) {
+      ptx::mbar_init(&p_full[i], 1);
+      ptx::mbar_init(&p_empty[i], 1);
+    }
+    for (int i = 0; i < ADA_NV; ++i) {
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], 1);
+    }
+  }
+  __syncthreads();
+
+  const float qscale = kLog2e * rsqrtf((float)d);
+  uint32_t gbase = 0;  // running tile sequence number (barrier phases)
+  for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    const sphkv_unit_t unit = p.units[u];
+    if (warp == 0) build_tiles(st, unit, TI, tiles, ntiles_s, lane);
+    // q rows for this group, prescaled into base-2 logit units, packed pairs
+    const float* qg = p.q + (size_t)unit.group * p.G * d;
+    for (int i = threadIdx.x; i < d * GP; i += blockDim.x) {
+      int j = i / GP, g2 = i % GP;
+      float a = (2 * g2 < p.G) ? qg[(size_t)(2 * g2) * d + j] * qscale : 0.f;
+      float b = (2 * g2 + 1 < p.G) ? qg[(size_t)(2 * g2 + 1) * d + j] * qscale : 0.f;
+      qs[i] = make_float2(a, b);
+    }
+    __syncthreads();
+    const int nt = *ntiles_s;
+
+    if (warp < ADA_NL) {
+      // ---------------- logit warps ----------------
+      for (int k = warp; k < nt; k += ADA_NL) {
+        const uint32_t gk = gbase + k;
+        const TileEntry te = tiles[k];
+        const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
+        const sphkv_page_t pg = st.pages[te.page];
+        // prefetch my next tile's code block into L2
+        if (k + ADA_NL < nt && lane == 0) {
+          const TileEntry tn = tiles[k + ADA_NL];
+          if ((tn.sub_off >> 24) == 0) {
+            const sphkv_page_t pn = st.pages[tn.page];
+            uint32_t bytes = (uint32_t)code_block_bytes(d, P, pn.abits, pn.rbits);
+            ptx::bulk_prefetch_l2(st.codes + pn.code_off, bytes);
+          }
+        }
+        const int ti = tier_index(st, pg.tier);
+        const int loff = p.lut_off[ti];
+        const float2* tl = loff >= 0 ? lut + loff : nullptr;
+        float lg[4][2 * GP];
+        ada_logit_dispatch<GP>(pg.abits, p, pg, sub, lane, qs, tl, lg);
+        int nvalid = pg.count - sub * TI - 4 * lane;
+        nvalid = nvalid < 0 ? 0 : (nvalid > 4 ? 4 : nvalid);
+        if (4 * lane >= TI) nvalid = 0;
+        if (p.logits_dbg != nullptr) {
+          float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 4 * lane) * p.G;
+          for (int kk = 0; kk < nvalid; ++kk)
+            for (int g = 0; g < p.G; ++g) dst[kk * p.G + g] = lg[kk][g] * (1.0f / kLog2e);
+        }
+        const int ps = gk % ADA_NS;
+        ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
+        write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, TI, lane, p.G, lg, nvalid);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
+      }
+    } else if (warp == ADA_NL) {
+      // ---------------- PV warp ----------------
+      PVState s;
+      pv_init(s);
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t gk = gbase + k;
+        const int vs = gk % ADA_NV, ps = gk % ADA_NS;
+        ptx::mbar_wait(&v_full[vs], (gk / ADA_NV) & 1);
+        ptx::mbar_wait(&p_full[ps], (gk / ADA_NS) & 1);
+        pv_tile(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes, p.prow_bytes, TI,
+                dvp, MT, p.G, lane);
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&p_empty[ps]);
+          ptx::mbar_arrive(&v_empty[vs]);
+        }
+      }
+      float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
+      pv_write(s, part, p.G, st.d_v, MT, lane);
+    } else {
+      // ---------------- producer ----------------
+      if (lane == 0) {
+        for (int k = 0; k < nt; ++k) {
+          const uint32_t gk = gbase + k;
+          const int vs = gk % ADA_NV;
+          ptx::mbar_wait(&v_empty[vs], ((gk / ADA_NV) & 1) ^ 1);
+          const TileEntry te = tiles[k];
+          const int sub = te.sub_off >> 24;
+          const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)sub * TI) * dvp;
+          ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
+          ptx::bulk_g2s(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs]);
+        }
+      }
+    }
+    gbase += nt;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Dense bf16 paged decode (baseline), same unit / partial contract
+// ---------------------------------------------------------------------------
+constexpr int DN_NL = 4;
+constexpr int DN_TI = 64;
+constexpr int DN_NK = 8;
+constexpr int DN_NV = 4;
+constexpr int DN_NS = 8;
+constexpr int DN_THREADS = (DN_NL + 2) * 32;
+
+struct DenseParams {
+  sphkv_dense_store_t st;
+  const float* q;
+  int G;
+  const sphkv_unit_t* units;
+  int n_units;
+  float* partials;
+  int dp, dvp;            // padded key / value widths
+  uint32_t smem_k, smem_v, smem_p, smem_bar;
+  int pslot_bytes, prow_bytes;
+};
+
+__global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParams p) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const sphkv_dense_store_t& st = p.st;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* kslots = smem + p.smem_k;
+  uint8_t* vslots = smem + p.smem_v;
+  uint8_t* pslots = smem + p.smem_p;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
+  uint64_t* k_full = bars;
+  uint64_t* k_empty = bars + DN_NK;
+  uint64_t* v_full = bars + 2 * DN_NK;
+  uint64_t* v_empty = v_full + DN_NV;
+  uint64_t* p_full = v_empty + DN_NV;
+  uint64_t* p_empty = p_full + DN_NS;
+  const int P = st.page_size, dp = p.dp, dvp = p.dvp, MT = dvp / 16, KT = dp / 16;
+  const uint32_t kbytes = (uint32_t)DN_TI * dp * 2, vbytes = (uint32_t)DN_TI * dvp * 2;
+  const int tiles_per_page = P / DN_TI;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < DN_NK; ++i) { ptx::mbar_init(&k_full[i], 1); ptx::mbar_init(&k_empty[i], 1); }
+    for (int i = 0; i < DN_NV; ++i) { ptx::mbar_init(&v_full[i], 1); ptx::mbar_init(&v_empty[i], 1); }
+    for (int i = 0; i < DN_NS; ++i) { ptx::mbar_init(&p_full[i], 1); ptx::mbar_init(&p_empty[i], 1); }
+  }
+  __syncthreads();
+  const float qscale = kLog2e * rsqrtf((float)st.d);
+  uint32_t gbase = 0;
+  for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+    const sphkv_unit_t unit = p.units[u];
+    const int t_begin = unit.ptr_begin * tiles_per_page;
+    int t_end = unit.ptr_end * tiles_per_page;
+    const int t_max = (st.tokens + DN_TI - 1) / DN_TI;
+    if (t_end > t_max) t_end = t_max;
+    const int nt = t_end > t_begin ? t_end - t_begin : 0;
+    const size_t gpage0 = (size_t)unit.group * st.n_pages_per_group;
+
+    if (warp < DN_NL) {
+      // q^T B-fragments in registers (bf16), g = lane / 4
+      uint32_t qb[8][2];
+      {
+        const int g = lane >> 2;
+        const float* qg = p.q + ((size_t)unit.group * p.G + g) * st.d;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int j = kk * 16 + h * 8 + 2 * (lane & 3);
+            float a = (g < p.G && j < st.d) ? qg[j] * qscale : 0.f;
+            float b = (g < p.G && j + 1 < st.d) ? qg[j + 1] * qscale : 0.f;
+            __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+            qb[kk][h] = *reinterpret_cast<uint32_t*>(&v);
+          }
+        }
+      }
+      const int nchunks = dp / 8, smask = (nchunks < 8 ? nchunks : 8) - 1;
+      for (int k = warp; k < nt; k += DN_NL) {
+        const uint32_t gk = gbase + k;
+        const int ks = gk % DN_NK, ps = gk % DN_NS;
+        ptx::mbar_wait(&k_full[ks], (gk / DN_NK) & 1);
+        const uint32_t kb = ptx::smem_u32(kslots + (size_t)ks * kbytes);
+        float c[DN_TI / 16][4];
+#pragma unroll
+        for (int mi = 0; mi < DN_TI / 16; ++mi) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) c[mi][r] = 0.f;
+          const int item = mi * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            if (kk < KT) {
+              int chunk = 2 * kk + (lane >> 4);
+              int sw = chunk ^ (item & smask);
+              uint32_t a0, a1, a2, a3;
+              ptx::ldsm_x4(kb + (item * dp + sw * 8) * 2, a0, a1, a2, a3);
+              ptx::mma_bf16(c[mi], a0, a1, a2, a3, qb[kk][0], qb[kk][1]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&k_empty[ks]);
+        // softmax over the tile per head column
+        const int tok0 = (t_begin + k) * DN_TI;
+        uint8_t* slot = pslots + ps * p.pslot_bytes;
+        ptx::mbar_wait(&p_empty[ps], ((gk / DN_NS) & 1) ^ 1);
+        float* hdr = reinterpret_cast<float*>(slot + 8 * p.prow_bytes);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int g = 2 * (lane & 3) + h;
+          float m = -INFINITY;
+#pragma unroll
+          for (int mi = 0; mi < DN_TI / 16; ++mi) {
+            int i0 = mi * 16 + (lane >> 2);
+            if (tok0 + i0 < st.tokens) m = fmaxf(m, c[mi][h]);
+            if (tok0 + i0 + 8 < st.tokens) m = fmaxf(m, c[mi][2 + h]);
+          }
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+          float s = 0.f;
+#pragma unroll
+          for (int mi = 0; mi < DN_TI / 16; ++mi) {
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+              int i0 = mi * 16 + (lane >> 2) + rr * 8;
+              float e = (tok0 + i0 < st.tokens) ? exp2f(c[mi][2 * rr + h] - m) : 0.f;
+              __half hv = __float2half_rn(e);
+              s += __half2float(hv);
+              if (g < p.G) *reinterpret_cast<__half*>(slot + g * p.prow_bytes + i0 * 2) = hv;
+            }
+          }
+          s += __shfl_xor_sync(0xffffffffu, s, 4);
+          s += __shfl_xor_sync(0xffffffffu, s, 8);
+          s += __shfl_xor_sync(0xffffffffu, s, 16);
+          if ((lane >> 2) == 0) {
+            hdr[g] = m;
+            hdr[8 + g] = s;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
+      }
+    } else if (warp == DN_NL) {
+      PVState s;
+      pv_init(s);
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t gk = gbase + k;
+        const int vs = gk % DN_NV, ps = gk % DN_NS;
+        ptx::mbar_wait(&v_full[vs], (gk / DN_NV) & 1);
+        ptx::mbar_wait(&p_full[ps], (gk / DN_NS) & 1);
+        pv_tile(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes, p.prow_bytes, DN_TI,
+                dvp, MT, p.G, lane);
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&p_empty[ps]);
+          ptx::mbar_arrive(&v_empty[vs]);
+        }
+      }
+      float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
+      pv_write(s, part, p.G, st.d_v, MT, lane);
+    } else if (lane == 0) {
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t gk = gbase + k;
+        const int ks = gk % DN_NK, vs = gk % DN_NV;
+        const size_t tile = (size_t)(t_begin + k);
+        const size_t item0 = gpage0 * P + tile * DN_TI;
+        ptx::mbar_wait(&k_empty[ks], ((gk / DN_NK) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&k_full[ks], kbytes);
+        ptx::bulk_g2s(kslots + (size_t)ks * kbytes, st.keys + item0 * dp, kbytes, &k_full[ks]);
+        ptx::mbar_wait(&v_empty[vs], ((gk / DN_NV) & 1) ^ 1);
+        ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
+        ptx::bulk_g2s(vslots + (size_t)vs * vbytes, st.values + item0 * dvp, vbytes, &v_full[vs]);
+      }
+    }
+    gbase += nt;
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LSE merge
+// ---------------------------------------------------------------------------
+__global__ void k_lse_merge(const float* __restrict__ partials, const int32_t* __restrict__ sb,
+                            int n_groups, int G, int d_v, float* __restrict__ out) {
+  const int gid = blockIdx.x;  // group * G + g
+  if (gid >= n_groups * G) return;
+  const int grp = gid / G, g = gid % G;
+  const int b = sb[grp], e = sb[grp + 1];
+  const int64_t stride = (int64_t)G * (d_v + 2);
+  float M = -INFINITY;
+  for (int s = b; s < e; ++s) M = fmaxf(M, partials[s * stride + g]);
+  float L = 0.f;
+  for (int s = b; s < e; ++s) {
+    float m = partials[s * stride + g];
+    if (m != -INFINITY) L += partials[s * stride + G + g] * exp2f(m - M);
+  }
+  for (int j = threadIdx.x; j < d_v; j += blockDim.x) {
+    float a = 0.f;
+    for (int s = b; s < e; ++s) {
+      float m = partials[s * stride + g];
+      if (m != -INFINITY) a += partials[s * stride + 2 * G + (int64_t)g * d_v + j] * exp2f(m - M);
+    }
+    out[(int64_t)gid * d_v + j] = (L > 0.f) ? a / L : 0.f;
+  }
+}
+
+}  // namespace sphkv
+
+using namespace sphkv;
+
+// ---------------------------------------------------------------------------
+// host entry points
+// ---------------------------------------------------------------------------
+static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+extern "C" int64_t sphkv_partial_floats(int G, int d_v) { return (int64_t)G * (d_v + 2); }
+
+template <int GP>
+static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
+  auto kern = k_ada_decode<GP>;
+  SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, ADA_THREADS, smem, stream>>>(p);
+  SPHKV_LAUNCH_CHECK();
+  return SPHKV_OK;
+}
+
+extern "C" int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
+                                const sphkv_unit_t* units, int n_units, float* partials,
+                                float* logits_dbg, const int64_t* dbg_offsets, int grid,
+                                cudaStream_t stream) {
+  if (!st || !q || !units || !partials) return fail(SPHKV_E_VALUE, "null argument");
+  if (G < 1 || G > 8) return fail(SPHKV_E_UNSUPPORTED, "GQA group size %d outside [1, 8]", G);
+  if (st->d < 3 || st->d > 256) return fail(SPHKV_E_UNSUPPORTED, "d=%d outside [3, 256]", st->d);
+  if (st->d_v < 1 || st->d_v > 128) return fail(SPHKV_E_UNSUPPORTED, "d_v=%d outside [1, 128]", st->d_v);
+  if (st->page_size % 32 != 0 || st->page_size < 32 || st->page_size > 1024 ||
+      (st->page_size > 128 && st->page_size % 128 != 0))
+    return fail(SPHKV_E_UNSUPPORTED, "page_size=%d unsupported", st->page_size);
+  if (logits_dbg && !dbg_offsets) return fail(SPHKV_E_VALUE, "dbg offsets missing");
+  for (int t = 1; t < st->n_tiers; ++t)
+    if (st->tiers[t].angle_bits > 16 || st->tiers[t].radius_bits > 16)
+      return fail(SPHKV_E_UNSUPPORTED, "tier %d: code widths above 16 bits", st->tiers[t].id);
+  if (n_units == 0) return SPHKV_OK;
+
+  AdaParams p;
+  memset(&p, 0, sizeof(p));
+  p.st = *st;
+  p.q = q;
+  p.G = G;
+  p.units = units;
+  p.n_units = n_units;
+  p.partials = partials;
+  p.logits_dbg = logits_dbg;
+  p.dbg_off = dbg_offsets;
+  p.TI = st->page_size < ADA_TI ? st->page_size : ADA_TI;
+  p.dvp = (st->d_v + 15) / 16 * 16;
+  // LUTs for the narrowest tiers first until the budget is used
+  int used = 0;
+  for (int t = 0; t < SPHKV_MAX_TIERS; ++t) p.lut_off[t] = -1;
+  for (int pass_b = 1; pass_b <= LUT_MAX_BITS; ++pass_b)
+    for (int t = 1; t < st->n_tiers; ++t)
+      if (st->tiers[t].angle_bits == pass_b && used + (1 << pass_b) <= LUT_BUDGET) {
+        p.lut_off[t] = used;
+        used += 1 << pass_b;
+      }
+  p.lut_entries = used;
+  const int GP = (G + 1) / 2;
+  size_t off = align_up((size_t)used * 8, 128);
+  p.smem_q = (uint32_t)off;
+  off = align_up(off + (size_t)st->d * GP * 8, 128);
+  p.smem_tiles = (uint32_t)off;
+  off = align_up(off + MAX_UNIT_TILES * sizeof(TileEntry) + 16, 128);
+  p.prow_bytes = p.TI * 2 + PROW_PAD;
+  p.pslot_bytes = (int)align_up(8 * p.prow_bytes + 64, 128);
+  p.smem_p = (uint32_t)off;
+  off += (size_t)ADA_NS * p.pslot_bytes;
+  off = align_up(off, 1024);
+  p.smem_v = (uint32_t)off;
+  off += (size_t)ADA_NV * p.TI * p.dvp * 2;
+  p.smem_bar = (uint32_t)off;
+  off += (2 * ADA_NS + 2 * ADA_NV) * 8;
+  size_t smem = off;
+  if (smem > 227 * 1024) return fail(SPHKV_E_UNSUPPORTED, "ADA smem %zu exceeds 227 KB", smem);
+  if (grid <= 0) grid = SM_COUNT;
+  if (grid > n_units) grid = n_units;
+  switch (GP) {
+    case 1: return launch_ada<1>(p, smem, grid, stream);
+    case 2: return launch_ada<2>(p, smem, grid, stream);
+    case 3: return launch_ada<3>(p, smem, grid, stream);
+    default: return launch_ada<4>(p, smem, grid, stream);
+  }
+}
+
+extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,
+                                  const sphkv_unit_t* units, int n_units, float* partials,
+                                  int grid, cudaStream_t stream) {
+  if (!st || !q || !units || !partials) return fail(SPHKV_E_VALUE, "null argument");
+  if (G < 1 || G > 8) return fail(SPHKV_E_UNSUPPORTED, "GQA group size %d outside [1, 8]", G);
+  if (st->d > 128 || st->d_v > 128) return fail(SPHKV_E_UNSUPPORTED, "d/d_v above 128");
+  if (st->page_size % DN_TI != 0) return fail(SPHKV_E_UNSUPPORTED, "page_size %% 64 != 0");
+  if (n_units == 0) return SPHKV_OK;
+  DenseParams p;
+  memset(&p, 0, sizeof(p));
+  p.st = *st;
+  p.q = q;
+  p.G = G;
+  p.units = units;
+  p.n_units = n_units;
+  p.partials = partials;
+  p.dp = (st->d + 15) / 16 * 16;
+  p.dvp = (st->d_v + 15) / 16 * 16;
+  p.prow_bytes = DN_TI * 2 + PROW_PAD;
+  p.pslot_bytes = (int)align_up(8 * p.prow_bytes + 64, 128);
+  size_t off = 0;
+  p.smem_k = 0;
+  off += (size_t)DN_NK * DN_TI * p.dp * 2;
+  off = align_up(off, 1024);
+  p.smem_v = (uint32_t)off;
+  off += (size_t)DN_NV * DN_TI * p.dvp * 2;
+  off = align_up(off, 128);
+  p.smem_p = (uint32_t)off;
+  off += (size_t)DN_NS * p.pslot_bytes;
+  off = align_up(off, 8);
+  p.smem_bar = (uint32_t)off;
+  off += (2 * DN_NK + 2 * DN_NV + 2 * DN_NS) * 8;
+  size_t smem = off;
+  if (smem > 227 * 1024) return fail(SPHKV_E_UNSUPPORTED, "dense smem %zu exceeds 227 KB", smem);
+  SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  if (grid <= 0) grid = SM_COUNT;
+  if (grid > n_units) grid = n_units;
+  k_dense_decode<<<grid, DN_THREADS, smem, stream>>>(p);
+  SPHKV_LAUNCH_CHECK();
+  return SPHKV_OK;
+}
+
+extern "C" int sphkv_lse_merge(const float* partials, const int32_t* slot_begin, int n_groups,
+                               int G, int d_v, float* out, cudaStream_t stream) {
+  if (!partials || !slot_begin || !out) return fail(SPHKV_E_VALUE, "null argument");
+  if (n_groups == 0) return SPHKV_OK;
+  int threads = d_v >= 128 ? 128 : ((d_v + 31) / 32) * 32;
+  k_lse_merge<<<n_groups * G, threads, 0, stream>>>(partials, slot_begin, n_groups, G, d_v, out);
+  SPHKV_LAUNCH_CHECK();
+  return SPHKV_OK;
+}

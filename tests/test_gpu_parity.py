@@ -1,0 +1,382 @@
+"""GPU parity: CUDA path (through the C ABI) vs the reference's golden vectors
+and the CPU oracle on identical inputs.
+
+Bit-exact: radii, angle/radius codes, page streams, SPHKV1 bytes, appends,
+RDR best tier / score / nu / allocations.  Tolerance (north_star): logits
+max |dl| / max(1, |l|) <= 1e-3 and outputs ||do||_inf / ||o||_inf <= 1e-3.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+from oracle import sphkv_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_TOL = 1e-3
+OUT_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def sk():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_18856_b200 as sk
+    from paper_2605_18856_b200 import _lib
+
+    _lib.require_gpu()
+    return sk
+
+
+def table(sk, rows, eps=None):
+    t = sk.TierTable(tuple(sk.TierSpec(*map(int, r)) for r in rows))
+    for k, s in enumerate(t.non_drop):
+        e = eps[k] if eps is not None else (0.01 / (k + 1), 0.005 / (k + 1))
+        t.eps_theta[s.id], t.eps_r[s.id] = float(e[0]), float(e[1])
+    return t
+
+
+def boundary_distance(angle, bits, polar):
+    step = O.polar_step(bits) if polar else O.circular_step(bits)
+    x = angle / step
+    return abs(x - math.floor(x) - 0.5)
+
+
+# ---------------------------------------------------------------------------
+# encoder / quantizer
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("d", [2, 3, 8, 64, 128])
+def test_encoder_matches_golden(sk, golden, d):
+    g = golden("codec")
+    r, ang = sk.encode_batch(g[f"d{d}_keys"])
+    assert np.array_equal(r.view(np.uint64), g[f"d{d}_radii"].view(np.uint64)), "radii bits"
+    want = g[f"d{d}_angles"]
+    ulp = np.abs(ang - want) / np.maximum(np.spacing(np.abs(want)), 1e-300)
+    assert np.all((ang == want) | (ulp <= 4)), f"max ulp {ulp.max()}"
+    flips = 0
+    for b in (1, 2, 4, 6, 7, 8, 12, 15, 16):
+        codes = sk.quantize_angles(ang, b).astype(np.uint16)
+        bad = np.argwhere(codes != g[f"d{d}_codes_b{b}"])
+        for i, j in bad:  # a flip is only legal on a rounding boundary (libm ulp tie)
+            assert boundary_distance(want[i, j], b, j < d - 2) < 1e-9, (b, i, j)
+        flips += len(bad)
+    assert flips <= 2
+
+
+@pytest.mark.parametrize("d", [2, 8, 64, 128])
+def test_quantizer_bit_exact_on_reference_angles(sk, golden, d):
+    g = golden("codec")
+    for b in (1, 2, 4, 6, 7, 8, 12, 15, 16):
+        codes = sk.quantize_angles(g[f"d{d}_angles"], b).astype(np.uint16)
+        assert np.array_equal(codes, g[f"d{d}_codes_b{b}"]), b
+
+
+def test_angles_from_unit_and_zero_vector(sk):
+    s = sk.to_spherical(np.zeros(4))
+    assert s.radius == 0.0 and np.all(s.angles == 0.0)
+    s = sk.to_spherical(np.array([0.0, 2.0]))
+    assert s.radius == pytest.approx(2.0) and s.angles == pytest.approx([math.pi / 2])
+    u = np.random.default_rng(0).standard_normal((50, 9))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    assert np.allclose(sk.angles_from_unit(u), O.angles_from_unit(u), rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------------------------------------
+# packer / export / appends
+# ---------------------------------------------------------------------------
+
+CASES = ["small", "panel64", "panel128", "odd"]
+
+
+def pack_case(sk, g, name, from_keys=False):
+    p = name + "_"
+    L, H, T, d, dv, P, G = (int(x) for x in g[p + "dims"])
+    tiers = table(sk, g[p + "tiers"])
+    asg = sk.TierAssignment(g[p + "z"], g[p + "tier"], g[p + "protected"])
+    if P % 32:
+        pytest.skip("device pages are multiples of 32 items")
+    if not from_keys:
+        st = sk.pack_pages_arrays(asg, g[p + "radii"], g[p + "angles"], g[p + "values"], tiers, P)
+    else:
+        st = sk.PagedStore(tiers, L, H, d, dv, P, capacity_tokens=T)
+        sk.pack_device(st, keys=g[p + "keys"].reshape(-1, d), radii=g[p + "radii"].reshape(-1),
+                       values=g[p + "values"].reshape(-1, dv), z=g[p + "z"].reshape(-1),
+                       tier=g[p + "tier"].reshape(-1), protect=g[p + "protected"].reshape(-1),
+                       tokens=T)
+    return st, tiers, (L, H, T, d, dv, P, G)
+
+
+def check_store_bytes(st, g, prefix):
+    pages = st.pages
+    assert len(pages) == int(g[prefix + "n_pages"])
+    meta = np.array([[p.tier.id, p.layer, p.head, p.count] for p in pages]).reshape(-1, 4)
+    assert np.array_equal(meta, g[prefix + "meta"])
+    assert np.array_equal(np.array([p.radius_scale for p in pages]), g[prefix + "scales"])
+    a = [p.angle_stream() for p in pages]
+    assert np.array_equal(np.concatenate(a) if a else np.zeros(0, np.uint8), g[prefix + "astream"])
+    r = [p.radius_stream() for p in pages]
+    assert np.array_equal(np.concatenate(r) if r else np.zeros(0, np.uint8), g[prefix + "rstream"])
+    br = st.resident_breakdown()
+    assert [br.payload_bytes, br.header_bytes, br.ptr_bytes, br.tag_bytes, br.prot_bytes,
+            br.frag_bytes, br.total] == list(g[prefix + "resident"])
+    blob = np.frombuffer(st.to_bytes(), dtype=np.uint8)
+    assert np.array_equal(blob, g[prefix + "sphkv1"])
+    assert blob.size == br.total - br.frag_bytes
+    st.check_invariants()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pack_pages_bit_exact(sk, golden, name):
+    g = golden("store")
+    st, *_ = pack_case(sk, g, name)
+    check_store_bytes(st, g, name + "_pack_")
+    # full pages: the device code block IS the reference stream (stride = P)
+    P = st.page_size
+    for p in st.pages:
+        if p.count == P:
+            row = st._host()[1][p.index]
+            nbytes = len(p.angle_stream())
+            dev = st.t_codes[int(row["code_off"]): int(row["code_off"]) + nbytes].cpu().numpy()
+            assert np.array_equal(dev, p.angle_stream())
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_pack_from_dense_keys(sk, golden, name):
+    g = golden("store")
+    st, *_ = pack_case(sk, g, name, from_keys=True)
+    check_store_bytes(st, g, name + "_pack_")
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_appends_bit_exact(sk, golden, name):
+    g = golden("store")
+    st, tiers, (L, H, T, d, dv, P, G) = pack_case(sk, g, name)
+    p = name + "_"
+    for i in range(g[p + "app_radii"].size):
+        l, h = (int(x) for x in g[p + "app_lh"][i])
+        key = sk.SphericalKey(float(g[p + "app_radii"][i]), g[p + "app_angles"][i])
+        st.append_item(l, h, key, g[p + "app_values"][i], int(g[p + "app_tier"][i]),
+                       protected=bool(g[p + "app_prot"][i]), token_id=T + i)
+    check_store_bytes(st, g, p + "app_")
+
+
+# ---------------------------------------------------------------------------
+# attend
+# ---------------------------------------------------------------------------
+
+def assert_attend_close(lg, out, want_lg, want_out):
+    assert lg.shape == want_lg.shape
+    if want_lg.size:
+        err = np.max(np.abs(lg - want_lg) / np.maximum(1.0, np.abs(want_lg)))
+        assert err <= LOGIT_TOL, err
+    den = max(np.max(np.abs(want_out)), 1e-30)
+    assert np.max(np.abs(out - want_out)) / den <= OUT_TOL
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_ada_attend_matches_reference_golden(sk, golden, name):
+    g = golden("store")
+    st, tiers, (L, H, T, d, dv, P, G) = pack_case(sk, g, name)
+    p = name + "_"
+    lens = g[p + "logits_len"]
+    off = k = 0
+    for l in range(L):
+        for h in range(H):
+            lg, out = sk.decode.attend_heads(st, l, h, g[p + "q"][l, h])
+            for gi in range(G):
+                want = g[p + "logits"][off: off + lens[k]]
+                assert_attend_close(lg[gi], out[gi], want, g[p + "outputs"][k])
+                off += lens[k]
+                k += 1
+
+
+def test_empty_head_yields_zero_output(sk):
+    tiers = table(sk, [(0, 0, 0, 0), (1, 4, 6, 0)])
+    L, H, T, d = 1, 2, 64, 8
+    rng = np.random.default_rng(0)
+    keys = rng.standard_normal((L, H, T, d))
+    r, a = O.encode_batch(keys.reshape(-1, d))
+    z = np.ones((L, H, T), np.int8)
+    z[0, 1] = 0
+    tier = z.astype(np.int16)
+    asg = sk.TierAssignment(z, tier, np.zeros((L, H, T), bool))
+    st = sk.pack_pages_arrays(asg, r.reshape(L, H, T), a.reshape(L, H, T, d - 1),
+                              rng.standard_normal((L, H, T, d)), tiers, 32)
+    lg, out = sk.decode.attend_heads(st, 0, 1, rng.standard_normal((3, d)))
+    assert lg.shape == (3, 0) and np.all(out == 0)
+    assert sk.angle_logits(np.ones(d), st, 0, 1).size == 0
+
+
+def test_split_merge_equals_single_pass(sk):
+    """Many page-range splits merged by the LSE kernel == one softmax (decode.py:347-354)."""
+    import torch
+
+    wl = sk.synth.generate(1, 1, 2, 4, 4096, 64, seed=3)
+    tiers = table(sk, [(0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8), (3, 12, 14, 8)])
+    st = sk.PagedStore(tiers, 1, 2, 64, 64, 128, capacity_tokens=4096)
+    n = wl.groups * wl.tokens
+    rng = np.random.default_rng(1)
+    tier = rng.choice([0, 1, 2, 3], n, p=[0.1, 0.4, 0.4, 0.1]).astype(np.int16)
+    radii = torch.empty(n, dtype=torch.float64, device="cuda")
+    from paper_2605_18856_b200 import _lib
+    _lib.check(_lib.lib().sphkv_encode_radii(wl.keys.data_ptr(), _lib.BF16, n, 64,
+                                             radii.data_ptr(), _lib.stream_ptr()))
+    sk.pack_device(st, keys=wl.keys.view(-1, 64), radii=radii, values=wl.values.view(-1, 64),
+                   z=(tier != 0).astype(np.int8), tier=tier, protect=np.zeros(n, np.uint8),
+                   tokens=wl.tokens)
+    one = sk.ada_decode(st, wl.queries, sk.plan_store(st, grid=2, units_per_cta=1))
+    many = sk.ada_decode(st, wl.queries, sk.plan_store(st, grid=148, units_per_cta=4))
+    assert torch.allclose(one, many, rtol=2e-5, atol=2e-5)
+
+
+def test_config1_geometry_vs_oracle(sk):
+    """1 layer, 8 KV / 32 Q heads, d=128, T=8K, P=256, panel tiers, RDR at a
+    ~30% KV-byte reduction: page bytes exact, attend within tolerance."""
+    import torch
+    from paper_2605_18856_b200 import synth
+
+    H, G, T, d = 8, 4, 8192, 128
+    wl = synth.generate(1, 1, H, G, T, d, seed=0)
+    keys64 = wl.keys.double().cpu().numpy().reshape(-1, d)
+    r, ang = O.encode_batch(keys64)
+    eps = {1: (0.2, 0.03), 2: (0.06, 0.008), 3: (0.015, 0.002), 4: (0.008, 0.002),
+           5: (0.0005, 0.00005), 6: (0.00006, 0.00001)}
+    tiers = synth.panel_tiers(eps=eps)
+    tl = [(t.id, t.angle_bits, t.radius_bits, t.meta_bits) for t in tiers.tiers]
+    u_hat, s_hat, r_q = synth.features(wl)
+    seg = wl.segments
+    omega = np.array(synth.PANEL_OMEGA)
+    prot = np.zeros((1, H, T), bool)
+    sc = O.score_states(r.reshape(1, H, T), u_hat.reshape(1, H), s_hat.reshape(1, H), r_q, omega,
+                        seg, 1.0, 1.0, tl, eps, synth.PANEL_LAMBDA, prot, d)
+    dense_bits = H * T * d * 16
+    z, tier = O.allocate_greedy(sc["best_tier"], sc["nu"], prot, int(0.3217 * dense_bits), tl, d)
+    vals = wl.values.float().cpu().numpy().reshape(1, H, T, d).astype(np.float64)
+    ost = O.pack_pages(tl, z, tier, prot, r.reshape(1, H, T), ang.reshape(1, H, T, d - 1),
+                       vals, 256)
+    st = sk.PagedStore(tiers, 1, H, d, d, 256, capacity_tokens=T)
+    sk.pack_device(st, keys=wl.keys.view(-1, d), radii=r, values=wl.values.view(-1, d),
+                   z=z.reshape(-1), tier=tier.reshape(-1), protect=prot.reshape(-1), tokens=T)
+    assert st.n_pages == len(ost.pages)
+    assert np.frombuffer(st.to_bytes(), np.uint8).tobytes() == ost.to_bytes()
+    # attend: every (kv head, q head)
+    q = wl.queries.double().cpu().numpy()
+    lgbuf = torch.zeros(st.retained_count() * G, dtype=torch.float32, device="cuda")
+    plan = sk.plan_store(st)
+    out = sk.ada_decode(st, wl.queries, plan, logits=lgbuf).double().cpu().numpy()
+    lg_all = lgbuf.double().cpu().numpy()
+    cache = O.FeatureCache()
+    off = 0
+    for h in range(H):
+        rq, qf = O.query_features(q[h])
+        n = int(plan.group_items[h])
+        lg = lg_all[off * G: (off + n) * G].reshape(n, G)
+        for gi in range(G):
+            want_lg, want_out = O.head_attend(ost, 0, h, rq[gi], qf[gi], cache)
+            assert_attend_close(lg[:, gi], out[h * G + gi], want_lg, want_out)
+        off += n
+
+
+# ---------------------------------------------------------------------------
+# dense baseline
+# ---------------------------------------------------------------------------
+
+def test_dense_decode_vs_oracle(sk):
+    import torch
+    from paper_2605_18856_b200 import synth
+
+    wl = synth.generate(1, 2, 2, 4, 3000, 128, seed=5)
+    ds = sk.DenseStore(2, 2, 128, 128, 256)
+    ds.bulk_load(wl.keys, wl.values)
+    out = sk.dense_decode(ds, wl.queries).double().cpu().numpy()
+    keys = wl.keys.double().cpu().numpy()
+    vals = wl.values.double().cpu().numpy()
+    q = wl.queries.double().cpu().numpy()
+    for g in range(wl.groups):
+        for gi in range(4):
+            _, want = O.dense_attend(q[g, gi], keys[g], vals[g])
+            err = np.max(np.abs(out[g * 4 + gi] - want)) / np.max(np.abs(want))
+            assert err <= 5e-3, err  # bf16 K / q in the dense baseline
+
+
+# ---------------------------------------------------------------------------
+# RDR
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("ci", range(6))
+def test_rdr_bit_exact(sk, golden, ci):
+    g = golden("rdr")
+    p = f"c{ci}_"
+    L, H, T, d = (int(x) for x in g[p + "dims"])
+    tiers = table(sk, g[p + "tiers"], g[p + "eps"])
+    r_q, lam, at, ar = g[p + "scalars"]
+    feat = sk.ControllerFeatures(u_hat=g[p + "u_hat"], s_hat=g[p + "s_hat"], r_q=float(r_q),
+                                 omega=g[p + "omega"], alpha_theta=float(at), alpha_r=float(ar),
+                                 segments=g[p + "seg"], prefill=T)
+    sc = sk.score_states(g[p + "radii"], feat, tiers, float(lam), g[p + "prot"], d)
+    assert np.array_equal(sc.best_tier, g[p + "best_tier"])
+    for key in ("score", "nu", "d_drop"):
+        assert np.array_equal(getattr(sc, key).view(np.uint64), g[p + key].view(np.uint64)), key
+    for bi, b in enumerate(g[p + "budgets"]):
+        asg = sk.allocate_greedy(sc, g[p + "prot"], int(b), tiers, d)
+        assert np.array_equal(asg.tier, g[p + f"greedy_{bi}_tier"]), ("greedy", bi)
+        start = sk.full_best_tier_assignment(sc, g[p + "prot"], tiers)
+        want = g[p + f"down_{bi}_tier"]
+        if np.all(want == -1):
+            with pytest.raises(sk.InfeasibleProtectionError):
+                sk.downtier_before_drop(start, sc, int(b), tiers, d)
+        else:
+            assert np.array_equal(sk.downtier_before_drop(start, sc, int(b), tiers, d).tier, want)
+
+
+def test_greedy_large_random_vs_oracle(sk):
+    """Exact parallel greedy vs the sequential oracle on 200K states with ties."""
+    rng = np.random.default_rng(11)
+    L, H, T, d = 2, 4, 25000, 128
+    tl = [tuple(x) for x in ((0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8), (3, 6, 8, 8),
+                             (4, 7, 8, 8), (5, 12, 14, 8), (6, 15, 16, 8))]
+    eps = {k: (0.3 / k ** 2, 0.05 / k ** 2) for k in range(1, 7)}
+    tiers = table(sk, tl, [eps[k] for k in range(1, 7)])
+    radii = np.round(rng.uniform(0.2, 3.0, (L, H, T)), 2)  # many exact nu ties
+    seg = rng.integers(0, 3, T).astype(np.int8)
+    u_hat, s_hat = rng.uniform(0.2, 1, (L, H)), rng.uniform(0, 0.8, (L, H))
+    prot = rng.random((L, H, T)) < 0.01
+    feat = sk.ControllerFeatures(u_hat=u_hat, s_hat=s_hat, r_q=30.0, omega=np.array([0.02, 2, 1.0]),
+                                 alpha_theta=1.0, alpha_r=1.0, segments=seg, prefill=T)
+    sc = sk.score_states(radii, feat, tiers, 3e-5, prot, d)
+    osc = O.score_states(radii, u_hat, s_hat, 30.0, np.array([0.02, 2, 1.0]), seg, 1.0, 1.0, tl,
+                         eps, 3e-5, prot, d)
+    assert np.array_equal(sc.nu.view(np.uint64), osc["nu"].view(np.uint64))
+    full = sum(O.rate_bits(tl[int(t)], d) for t in osc["best_tier"].ravel())
+    for frac in (0.05, 0.3217, 0.8):
+        b = int(frac * full)
+        asg = sk.allocate_greedy(sc, prot, b, tiers, d)
+        _, want = O.allocate_greedy(osc["best_tier"], osc["nu"], prot, b, tl, d)
+        assert np.array_equal(asg.tier, want), frac
+        z0, t0 = O.full_best_tier(osc["best_tier"], prot, tl)
+        _, want_d = O.downtier_before_drop(z0, t0, osc["nu"], prot, b, tl, d)
+        got_d = sk.downtier_before_drop(sk.full_best_tier_assignment(sc, prot, tiers), sc, b, tiers, d)
+        assert np.array_equal(got_d.tier, want_d), frac
+
+
+def test_scalar_append_scoring_matches_golden(sk, golden):
+    g = golden("rdr")
+    for ci in range(6):
+        p = f"c{ci}_"
+        L, H, T, d = (int(x) for x in g[p + "dims"])
+        tiers = table(sk, g[p + "tiers"], g[p + "eps"])
+        r_q, lam, at, ar = g[p + "scalars"]
+        feat = sk.ControllerFeatures(u_hat=g[p + "u_hat"], s_hat=g[p + "s_hat"], r_q=float(r_q),
+                                     omega=g[p + "omega"], alpha_theta=float(at),
+                                     alpha_r=float(ar), segments=g[p + "seg"], prefill=T)
+        for f, tid, s, nu in g[p + "scalar"]:
+            l, h, i = np.unravel_index(int(f), (L, H, T))
+            key = sk.SphericalKey(float(g[p + "radii"][l, h, i]), np.zeros(d - 1))
+            got = sk.score_and_best_tier(sk.StateId(int(l), int(h), int(i)), key, feat, tiers,
+                                         float(lam), protected=bool(g[p + "prot"][l, h, i]))
+            assert got[0] == int(tid) and got[1] == s and got[2] == nu
