@@ -92,6 +92,9 @@ typedef struct {
   uint8_t* protect;           /* [max_pages][P]                               */
   int64_t* token_ids;         /* [max_pages][P]                               */
   uint64_t* counters;         /* [0]=n_pages [1]=code bytes used (device)     */
+  float* lut;                 /* polar (cos, sin) tables, filled by
+                                 sphkv_store_build_lut; NULL -> computed in-kernel */
+  int32_t lut_off[SPHKV_MAX_TIERS];  /* float2 offset per tier index, -1 = none */
 } sphkv_store_t;
 
 /* Dense bf16-K / fp16-V paged store used by the dense baseline kernel
@@ -177,6 +180,12 @@ int sphkv_rdr_downtier(const int16_t* best_tier, const double* nu,
                        int16_t* tier, cudaStream_t stream);
 
 /* ---- paged store (store.py:214-482) ------------------------------------- */
+
+/* Fill st->lut (caller-allocated, sphkv_lut_floats() floats) and st->lut_off
+ * with fp32-rounded fp64 (cos, sin) of every polar grid point of each tier
+ * whose angle width fits the shared-memory LUT budget. */
+int64_t sphkv_lut_floats(const sphkv_store_t* st);
+int sphkv_store_build_lut(sphkv_store_t* st, cudaStream_t stream);
 
 /* Reset counters / pointer lists of a store (pools are zeroed by caller). */
 int sphkv_store_reset(const sphkv_store_t* st, cudaStream_t stream);

@@ -14,7 +14,7 @@ from ctypes import c_double, c_int, c_int32, c_int64, c_uint64, c_void_p
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsphkv_b200.so")
+LIB_PATH = os.environ.get("SPHKV_LIB") or os.path.join(HERE, "libsphkv_b200.so")
 
 SPHKV_OK = 0
 SPHKV_E_VALUE = 1
@@ -44,7 +44,8 @@ class CStore(ctypes.Structure):
                 ("code_cap", c_uint64), ("tiers", CTier * MAX_TIERS),
                 ("pages", c_void_p), ("ptr", c_void_p), ("ptr_len", c_void_p),
                 ("group_last", c_void_p), ("codes", c_void_p), ("values", c_void_p),
-                ("protect", c_void_p), ("token_ids", c_void_p), ("counters", c_void_p)]
+                ("protect", c_void_p), ("token_ids", c_void_p), ("counters", c_void_p),
+                ("lut", c_void_p), ("lut_off", c_int32 * MAX_TIERS)]
 
 
 class CDenseStore(ctypes.Structure):
@@ -80,6 +81,8 @@ def _declare(lib):
         "sphkv_rdr_allocate_greedy": (c_int, [vp, vp, vp, i64, vp, i, i, i64, vp, vp, vp, vp]),
         "sphkv_rdr_downtier": (c_int, [vp, vp, vp, i64, vp, i, i, i64, vp, vp, vp, vp]),
         "sphkv_store_reset": (c_int, [vp, vp]),
+        "sphkv_lut_floats": (c_int64, [vp]),
+        "sphkv_store_build_lut": (c_int, [vp, vp]),
         "sphkv_pack_pages": (c_int, [vp, vp, i, vp, vp, vp, vp, vp, vp, i, vp, i64, vp]),
         "sphkv_pack_workspace_bytes": (c_int64, [i, i, i, i]),
         "sphkv_append": (c_int, [vp, vp, i, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

@@ -56,7 +56,9 @@ __host__ __device__ inline uint64_t angle_row_bytes(int P, int abits) {
 // Value-pool element offset (in fp16 elements) of (item i, column e) inside a
 // page: 16-byte chunks XOR-swizzled by (i & 7) -- see sphkv_b200.h.
 __host__ __device__ inline int vswz(int i, int e, int d_v) {
-  int chunk = (e >> 3) ^ (i & 7);
+  const int nchunks = d_v >> 3;  // d_v is padded to a multiple of 16
+  const int mask = (nchunks < 8 ? nchunks : 8) - 1;
+  int chunk = (e >> 3) ^ (i & mask);
   return i * d_v + chunk * 8 + (e & 7);
 }
 

@@ -18,21 +18,21 @@
 //   warp NL        PV warp: V^T (ldmatrix.trans of the TMA-staged, swizzled
 //                  fp16 V tile) x P (fp16) on mma.sync, fp32 accumulate,
 //                  online-softmax combine across tiles, writes the partial.
-//   warp NL+1      producer: 1-D TMA bulk copies of V tiles into a ring.
+//                  Lane 0 also issues the 1-D TMA bulk copies of V tiles into a
+//                  4-slot ring (evict_first), NV tiles ahead of consumption.
 #include "common.cuh"
 #include "ptx.cuh"
+#include "ada_tile.cuh"
 
 namespace sphkv {
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int ADA_NL = 8;          // logit warps
+constexpr int ADA_NL = 7;          // logit warps
 constexpr int ADA_TI = 128;        // items per tile (4 per lane)
 constexpr int ADA_NS = 16;         // P slots
 constexpr int ADA_NV = 4;          // V slots
-constexpr int ADA_THREADS = (ADA_NL + 2) * 32;
+constexpr int ADA_THREADS = (ADA_NL + 1) * 32;  // 8 warps -> up to 255 registers
 constexpr int MAX_UNIT_TILES = 1024;
-constexpr int LUT_MAX_BITS = 12;
-constexpr int LUT_BUDGET = 6144;   // float2 entries (48 KB)
 constexpr int PROW_PAD = 16;       // bytes of padding per P row (bank spread)
 
 struct AdaParams {
@@ -46,6 +46,7 @@ struct AdaParams {
   const int64_t* dbg_off;
   int lut_off[SPHKV_MAX_TIERS];   // float2 offset of each tier's polar LUT, -1 = none
   int lut_entries;
+  const float2* lut_global;       // prebuilt tables (sphkv_store_build_lut) or NULL
   int TI;                   // tile items (min(P, 128))
   int dvp;                  // d_v padded to 16
   uint32_t smem_q, smem_tiles, smem_p, smem_v, smem_bar;  // byte offsets
@@ -56,150 +57,6 @@ __device__ __forceinline__ int tier_index(const sphkv_store_t& st, int tier_id) 
   for (int i = 0; i < st.n_tiers; ++i)
     if (st.tiers[i].id == tier_id) return i;
   return 0;
-}
-
-// ---------------------------------------------------------------------------
-// logit tile: 4 consecutive items per lane, G heads (GP packed pairs)
-// ---------------------------------------------------------------------------
-template <int B>
-struct CodeWin {
-  static constexpr int MAXSH = (B % 2) ? 28 : ((B % 4) ? 24 : ((B % 8) ? 16 : 0));
-  static constexpr int WORDS = (4 * B <= 32 && MAXSH + 4 * B <= 32) ? 1
-                             : (MAXSH + 4 * B <= 64 ? 2 : 3);
-};
-
-template <int B>
-__device__ __forceinline__ void extract4(const uint32_t* __restrict__ row, int w, int sh,
-                                         uint32_t c[4]) {
-  constexpr uint32_t M = (B == 32) ? 0xffffffffu : ((1u << B) - 1u);
-  if constexpr (CodeWin<B>::WORDS == 1) {
-    uint32_t x = __ldg(row + w) >> sh;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = (x >> (k * B)) & M;
-  } else if constexpr (CodeWin<B>::WORDS == 2) {
-    uint32_t lo = __ldg(row + w), hi = __ldg(row + w + 1);
-    uint32_t a = __funnelshift_r(lo, hi, sh);
-    uint32_t b = sh ? (hi >> sh) : hi;
-    uint64_t y = ((uint64_t)b << 32) | a;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = (uint32_t)(y >> (k * B)) & M;
-  } else {
-    uint32_t w0 = __ldg(row + w), w1 = __ldg(row + w + 1), w2 = __ldg(row + w + 2);
-    uint32_t a = __funnelshift_r(w0, w1, sh);
-    uint32_t b = __funnelshift_r(w1, w2, sh);
-    uint64_t y = ((uint64_t)b << 32) | a;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) c[k] = (uint32_t)(y >> (k * B)) & M;
-  }
-}
-
-__device__ __forceinline__ uint32_t read_bits_g(const uint32_t* __restrict__ words, uint64_t bit,
-                                                int nbits) {
-  uint64_t w = bit >> 5;
-  int sh = (int)(bit & 31);
-  uint32_t lo = __ldg(words + w);
-  uint32_t hi = (sh + nbits > 32) ? __ldg(words + w + 1) : 0u;
-  uint32_t v = __funnelshift_r(lo, hi, sh);
-  return nbits >= 32 ? v : (v & ((1u << nbits) - 1u));
-}
-
-template <int B, int GP>
-__device__ __forceinline__ void ada_logit_tile(const AdaParams& p, const sphkv_page_t& pg, int sub,
-                                            int lane, const float2* __restrict__ qs,
-                                            const float2* __restrict__ lut,
-                                            float lg[4][2 * GP]) {
-  const sphkv_store_t& st = p.st;
-  const int d = st.d, P = st.page_size;
-  const int item0 = sub * p.TI + 4 * lane;
-  const uint32_t* base = reinterpret_cast<const uint32_t*>(st.codes + pg.code_off);
-  const int row_words = P * B / 32;
-  const uint32_t obit = (uint32_t)item0 * B;
-  const int w = (int)(obit >> 5), sh = (int)(obit & 31);
-
-  float prod[4];
-  ptx::f2 acc[4][GP];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    prod[k] = 1.0f;
-#pragma unroll
-    for (int g = 0; g < GP; ++g) acc[k][g] = ptx::f2_make(0.f, 0.f);
-  }
-  const float pstep = (float)(1.0 / (double)((1u << B) - 1u));
-
-#pragma unroll 4
-  for (int j = 0; j < d - 2; ++j) {
-    uint32_t c[4];
-    extract4<B>(base + (size_t)j * row_words, w, sh, c);
-    ptx::f2 qv[GP];
-#pragma unroll
-    for (int g = 0; g < GP; ++g) qv[g].v = *reinterpret_cast<const unsigned long long*>(&qs[j * GP + g]);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float cs, sn;
-      if (B <= LUT_MAX_BITS && lut != nullptr) {
-        float2 t = lut[c[k]];
-        cs = t.x;
-        sn = t.y;
-      } else {
-        sincospif((float)c[k] * pstep, &sn, &cs);
-      }
-      float f = prod[k] * cs;
-#pragma unroll
-      for (int g = 0; g < GP; ++g) acc[k][g] = ptx::f2_fma_s(f, qv[g], acc[k][g]);
-      prod[k] *= sn;
-    }
-  }
-  // circular last angle (row d-2): step 2*pi/2^B  ->  sincospi(code * 2^(1-B))
-  {
-    uint32_t c[4];
-    extract4<B>(base + (size_t)(d - 2) * row_words, w, sh, c);
-    ptx::f2 qa[GP], qb[GP];
-#pragma unroll
-    for (int g = 0; g < GP; ++g) {
-      qa[g].v = *reinterpret_cast<const unsigned long long*>(&qs[(d - 2) * GP + g]);
-      qb[g].v = *reinterpret_cast<const unsigned long long*>(&qs[(d - 1) * GP + g]);
-    }
-    const float cstep = ldexpf(1.0f, 1 - B);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      float sn, cs;
-      sincospif((float)c[k] * cstep, &sn, &cs);
-      float f0 = prod[k] * cs, f1 = prod[k] * sn;
-#pragma unroll
-      for (int g = 0; g < GP; ++g) {
-        acc[k][g] = ptx::f2_fma_s(f0, qa[g], acc[k][g]);
-        acc[k][g] = ptx::f2_fma_s(f1, qb[g], acc[k][g]);
-      }
-    }
-  }
-  // radii (row d-1 holds the radius stream)
-  const uint64_t rbit0 = (uint64_t)(d - 1) * P * B;
-  const int rb = pg.rbits;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    uint32_t rc = read_bits_g(base, rbit0 + (uint64_t)(item0 + k) * rb, rb);
-    float rr = (float)rc * pg.rscale;
-#pragma unroll
-    for (int g = 0; g < GP; ++g) {
-      lg[k][2 * g] = rr * ptx::f2_lo(acc[k][g]);
-      lg[k][2 * g + 1] = rr * ptx::f2_hi(acc[k][g]);
-    }
-  }
-}
-
-template <int GP>
-__device__ void ada_logit_dispatch(int B, const AdaParams& p, const sphkv_page_t& pg, int sub,
-                                   int lane, const float2* qs, const float2* lut,
-                                   float lg[4][2 * GP]) {
-  switch (B) {
-#define SPHKV_CASE(b) \
-  case b: ada_logit_tile<b, GP>(p, pg, sub, lane, qs, lut, lg); break;
-    SPHKV_CASE(1) SPHKV_CASE(2) SPHKV_CASE(3) SPHKV_CASE(4) SPHKV_CASE(5) SPHKV_CASE(6)
-    SPHKV_CASE(7) SPHKV_CASE(8) SPHKV_CASE(9) SPHKV_CASE(10) SPHKV_CASE(11) SPHKV_CASE(12)
-    SPHKV_CASE(13) SPHKV_CASE(14) SPHKV_CASE(15) SPHKV_CASE(16)
-#undef SPHKV_CASE
-    default: break;
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -394,17 +251,16 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   const uint32_t vbytes = (uint32_t)TI * dvp * 2;
 
   // polar LUTs (fp64 sincos rounded to fp32), barrier init
+  if (p.lut_global != nullptr) {
+    const float4* src = reinterpret_cast<const float4*>(p.lut_global);
+    float4* dst = reinterpret_cast<float4*>(lut);
+    for (int i = threadIdx.x; i < (p.lut_entries + 1) / 2; i += blockDim.x) dst[i] = __ldg(src + i);
+  } else
   for (int t = 0; t < st.n_tiers; ++t) {
     int off = p.lut_off[t];
     if (off < 0) continue;
     int b = st.tiers[t].angle_bits;
-    int n = 1 << b;
-    double step = kPi / (double)((1u << b) - 1u);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      double sn, cs;
-      sincos((double)i * step, &sn, &cs);
-      lut[off + i] = make_float2((float)cs, (float)sn);
-    }
+    for (int i = threadIdx.x; i < lut_float2s(b); i += blockDim.x) lut[off + i] = lut_slot(b, i);
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < ADA_NS; ++i) {
@@ -447,14 +303,15 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
           if ((tn.sub_off >> 24) == 0) {
             const sphkv_page_t pn = st.pages[tn.page];
             uint32_t bytes = (uint32_t)code_block_bytes(d, P, pn.abits, pn.rbits);
-            ptx::bulk_prefetch_l2(st.codes + pn.code_off, bytes);
+            ptx::bulk_prefetch_l2_hint(st.codes + pn.code_off, bytes, ptx::policy_evict_last());
           }
         }
         const int ti = tier_index(st, pg.tier);
         const int loff = p.lut_off[ti];
-        const float2* tl = loff >= 0 ? lut + loff : nullptr;
+        const uint32_t lut_s = (loff >= 0 ? loff : 0) * 8u;  // LUT region starts at smem[0]
         float lg[4][2 * GP];
-        ada_logit_dispatch<GP>(pg.abits, p, pg, sub, lane, qs, tl, lg);
+        ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, TI, pg, sub, lane, smem, p.smem_q,
+                               lut_s, loff >= 0, lg);
         int nvalid = pg.count - sub * TI - 4 * lane;
         nvalid = nvalid < 0 ? 0 : (nvalid > 4 ? 4 : nvalid);
         if (4 * lane >= TI) nvalid = 0;
@@ -469,8 +326,21 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
       }
-    } else if (warp == ADA_NL) {
-      // ---------------- PV warp ----------------
+    } else {
+      // ---------------- PV warp (also the V producer) ----------------
+      const uint64_t vpol = ptx::policy_evict_first();
+      auto issue_v = [&](int k) {
+        const uint32_t gk = gbase + k;
+        const int vs = gk % ADA_NV;
+        const TileEntry te = tiles[k];
+        const int sub = te.sub_off >> 24;
+        const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)sub * TI) * dvp;
+        ptx::fence_proxy_async();  // order this warp's earlier ldmatrix reads of the slot
+        ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
+        ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
+      };
+      if (lane == 0)
+        for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k);
       PVState s;
       pv_init(s);
       for (int k = 0; k < nt; ++k) {
@@ -483,25 +353,11 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         __syncwarp();
         if (lane == 0) {
           ptx::mbar_arrive(&p_empty[ps]);
-          ptx::mbar_arrive(&v_empty[vs]);
+          if (k + ADA_NV < nt) issue_v(k + ADA_NV);  // slot vs is free again
         }
       }
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
       pv_write(s, part, p.G, st.d_v, MT, lane);
-    } else {
-      // ---------------- producer ----------------
-      if (lane == 0) {
-        for (int k = 0; k < nt; ++k) {
-          const uint32_t gk = gbase + k;
-          const int vs = gk % ADA_NV;
-          ptx::mbar_wait(&v_empty[vs], ((gk / ADA_NV) & 1) ^ 1);
-          const TileEntry te = tiles[k];
-          const int sub = te.sub_off >> 24;
-          const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)sub * TI) * dvp;
-          ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
-          ptx::bulk_g2s(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs]);
-        }
-      }
     }
     gbase += nt;
     __syncthreads();
@@ -724,6 +580,49 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 extern "C" int64_t sphkv_partial_floats(int G, int d_v) { return (int64_t)G * (d_v + 2); }
 
+// narrowest tiers first until the shared-memory budget is used
+static int lut_layout(const sphkv_store_t* st, int off[SPHKV_MAX_TIERS]) {
+  int used = 0;
+  for (int t = 0; t < SPHKV_MAX_TIERS; ++t) off[t] = -1;
+  for (int pass_b = 1; pass_b <= LUT_MAX_BITS; ++pass_b)
+    for (int t = 1; t < st->n_tiers; ++t)
+      if (st->tiers[t].angle_bits == pass_b && used + lut_float2s(pass_b) <= LUT_BUDGET) {
+        off[t] = used;  // every table size is even -> 16-B aligned offsets
+        used += lut_float2s(pass_b);
+      }
+  return used;
+}
+
+namespace sphkv {
+__global__ void k_build_lut(sphkv_store_t st, int entries) {
+  for (int t = 0; t < st.n_tiers; ++t) {
+    int off = st.lut_off[t];
+    if (off < 0) continue;
+    int b = st.tiers[t].angle_bits;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < lut_float2s(b);
+         i += gridDim.x * blockDim.x) {
+      const float2 v = lut_slot(b, i);
+      st.lut[2 * (off + i)] = v.x;
+      st.lut[2 * (off + i) + 1] = v.y;
+    }
+  }
+}
+}  // namespace sphkv
+
+extern "C" int64_t sphkv_lut_floats(const sphkv_store_t* st) {
+  int off[SPHKV_MAX_TIERS];
+  return 2 * (int64_t)lut_layout(st, off) + 4;
+}
+
+extern "C" int sphkv_store_build_lut(sphkv_store_t* st, cudaStream_t stream) {
+  if (!st || !st->lut) return fail(SPHKV_E_VALUE, "store lut buffer missing");
+  int used = lut_layout(st, st->lut_off);
+  if (used == 0) return SPHKV_OK;
+  k_build_lut<<<16, 256, 0, stream>>>(*st, used);
+  SPHKV_LAUNCH_CHECK();
+  return SPHKV_OK;
+}
+
 template <int GP>
 static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
   auto kern = k_ada_decode<GP>;
@@ -762,16 +661,14 @@ extern "C" int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
   p.dbg_off = dbg_offsets;
   p.TI = st->page_size < ADA_TI ? st->page_size : ADA_TI;
   p.dvp = (st->d_v + 15) / 16 * 16;
-  // LUTs for the narrowest tiers first until the budget is used
-  int used = 0;
-  for (int t = 0; t < SPHKV_MAX_TIERS; ++t) p.lut_off[t] = -1;
-  for (int pass_b = 1; pass_b <= LUT_MAX_BITS; ++pass_b)
-    for (int t = 1; t < st->n_tiers; ++t)
-      if (st->tiers[t].angle_bits == pass_b && used + (1 << pass_b) <= LUT_BUDGET) {
-        p.lut_off[t] = used;
-        used += 1 << pass_b;
-      }
+  int used = lut_layout(st, p.lut_off);
   p.lut_entries = used;
+  p.lut_global = nullptr;
+  if (st->lut != nullptr) {
+    bool same = true;
+    for (int t = 0; t < SPHKV_MAX_TIERS; ++t) same = same && (st->lut_off[t] == p.lut_off[t]);
+    if (same) p.lut_global = reinterpret_cast<const float2*>(st->lut);
+  }
   const int GP = (G + 1) / 2;
   size_t off = align_up((size_t)used * 8, 128);
   p.smem_q = (uint32_t)off;

@@ -254,13 +254,15 @@ class PagedStore:
         self.t_ptr_len = torch.zeros(self.groups, dtype=torch.int32, device=dev)
         self.t_group_last = torch.full((self.groups * _lib.MAX_TIERS,), -1, dtype=torch.int32,
                                        device=dev)
-        self.t_codes = torch.zeros(self.code_cap, dtype=torch.uint8, device=dev)
+        # tail slack: the decode look-ahead may read a few rows past the last block
+        self.t_codes = torch.zeros(self.code_cap + 16384, dtype=torch.uint8, device=dev)
         self.t_values = torch.zeros(self.max_pages * page_size * self.dvp, dtype=torch.float16,
                                     device=dev)
         self.t_protect = torch.zeros(self.max_pages * page_size, dtype=torch.uint8, device=dev)
         self.t_token_ids = torch.full((self.max_pages * page_size,), -1, dtype=torch.int64,
                                       device=dev)
         self.t_counters = torch.zeros(4, dtype=torch.int64, device=dev)
+        self.t_lut = None
         self._host_cache = None
         self._rebuild_cstruct()
 
@@ -282,6 +284,19 @@ class PagedStore:
         c.token_ids = self.t_token_ids.data_ptr()
         c.counters = self.t_counters.data_ptr()
         self.cstruct = c
+        self._build_lut()
+
+    def _build_lut(self):
+        import torch
+
+        l = _lib.require_gpu()
+        c = self.cstruct
+        c.tiers = _lib.tiers_to_c(self.tiers)
+        n = l.sphkv_lut_floats(ctypes.byref(c))
+        if self.t_lut is None or self.t_lut.numel() < n:
+            self.t_lut = torch.zeros(n, dtype=torch.float32, device="cuda")
+        c.lut = self.t_lut.data_ptr()
+        _lib.check(l.sphkv_store_build_lut(ctypes.byref(c), _lib.stream_ptr()))
 
     @property
     def cptr(self):
@@ -470,7 +485,7 @@ class PagedStore:
             return out
 
         self.t_pages = extend(self.t_pages, max_pages * 32)
-        self.t_codes = extend(self.t_codes, max_pages * max_block + 256)
+        self.t_codes = extend(self.t_codes, max_pages * max_block + 256 + 16384)
         self.t_values = extend(self.t_values, max_pages * P * dvp)
         self.t_protect = extend(self.t_protect, max_pages * P)
         self.t_token_ids = extend(self.t_token_ids, max_pages * P, -1)
