@@ -17,33 +17,92 @@
 namespace sphkv {
 
 constexpr int LUT_MAX_BITS = 12;
-constexpr int LUT_BUDGET = 6144;  // float2 slots (48 KB of shared memory)
+constexpr int LUT_BUDGET_BYTES = 90 * 1024;
 
-// Narrow tiers look up a group of consecutive items' codes at once: for each
-// item pair the entry holds (cos a, cos b, sin a, sin b), so one LDS.128 feeds
-// packed FMUL2s.  GS = 4 codes per entry for B <= 2, 2 for B <= 4, else 1.
-__host__ __device__ constexpr int lut_group(int B) { return B <= 2 ? 4 : (B <= 4 ? 2 : 1); }
-__host__ __device__ constexpr int lut_float2s(int B) {
-  return (1 << (lut_group(B) * B)) * lut_group(B);
+// Polar (cos, sin) tables in shared memory, one per tier with B <= 12.
+//  * B <= 4: "pair" tables indexed by two consecutive items' codes (2B bits);
+//    an entry (cos a, cos b, sin a, sin b) is one LDS.128 feeding packed FMUL2.
+//  * 5 <= B <= 12: single-code tables, entry (cos, sin) = one LDS.64.
+// Random gathers from a small table bank-conflict heavily, so when the budget
+// allows a table is stored REP times interleaved: entry e of copy r lives at
+// (e * REP + r) * entry_bytes and lane L reads copy L % REP.  REP = 8 for
+// 16-byte entries (8 lanes per LDS.128 phase) and 16 for 8-byte entries
+// (16 lanes per LDS.64 phase), so every phase hits distinct banks and the
+// entry stride is 128 bytes either way.
+__host__ __device__ constexpr int lut_group(int B) { return B <= 4 ? 2 : 1; }
+__host__ __device__ constexpr int lut_entry_bytes(int B) { return 8 * lut_group(B); }
+__host__ __device__ constexpr int lut_rep(int B) { return lut_group(B) == 2 ? 8 : 16; }
+__host__ __device__ constexpr int lut_bytes(int B, bool repl) {
+  return (1 << (lut_group(B) * B)) * lut_entry_bytes(B) * (repl ? lut_rep(B) : 1);
 }
 
-// float2 slot s of the polar table of a B-bit tier (fp64 sincos rounded to fp32)
-__device__ inline float2 lut_slot(int B, int s) {
-  const int gs = lut_group(B);
-  const double step = kPi / (double)((1u << B) - 1u);
-  const uint32_t M = (1u << B) - 1u;
-  double sa, ca;
-  if (gs == 1) {
-    sincos((double)s * step, &sa, &ca);
-    return make_float2((float)ca, (float)sa);
+// Encoded per-tier table descriptor: (byte offset << 1) | replicated, or -1.
+__host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n_tiers,
+                                                int off[SPHKV_MAX_TIERS]) {
+  for (int t = 0; t < SPHKV_MAX_TIERS; ++t) off[t] = -1;
+  int minimal = 0;
+  for (int t = 1; t < n_tiers; ++t) {
+    const int b = tiers[t].angle_bits;
+    if (b <= LUT_MAX_BITS && minimal + lut_bytes(b, false) <= LUT_BUDGET_BYTES) {
+      minimal += lut_bytes(b, false);
+      off[t] = 0;  // has a table; placed below
+    }
   }
-  const int entry = s / gs, part = s % gs;
-  const int pp = part >> 1, h = part & 1;
-  const uint32_t a = (entry >> (2 * pp * B)) & M, b = (entry >> ((2 * pp + 1) * B)) & M;
-  double sb, cb;
-  sincos((double)a * step, &sa, &ca);
-  sincos((double)b * step, &sb, &cb);
-  return h == 0 ? make_float2((float)ca, (float)cb) : make_float2((float)sa, (float)sb);
+  bool repl[SPHKV_MAX_TIERS] = {};
+  int total = minimal;
+  for (int pass_b = 1; pass_b <= LUT_MAX_BITS; ++pass_b)  // narrow tiers first
+    for (int t = 1; t < n_tiers; ++t)
+      if (off[t] == 0 && tiers[t].angle_bits == pass_b) {
+        const int extra = lut_bytes(pass_b, true) - lut_bytes(pass_b, false);
+        if (total + extra <= LUT_BUDGET_BYTES) {
+          repl[t] = true;
+          total += extra;
+        }
+      }
+  int used = 0;  // every table size is a multiple of 16 bytes
+  for (int t = 1; t < n_tiers; ++t)
+    if (off[t] == 0) {
+      off[t] = (used << 1) | (repl[t] ? 1 : 0);
+      used += lut_bytes(tiers[t].angle_bits, repl[t]);
+    }
+  return used;
+}
+
+// Fill byte range [i*16, i*16+16) ... one entry copy per call: tier bits B,
+// entry e, copy r of a table starting at `dst`.
+__device__ inline void lut_write_entry(uint8_t* dst, int B, bool repl, int e, int r) {
+  const double step = kPi / (double)((1u << B) - 1u);
+  const int R = repl ? lut_rep(B) : 1;
+  float* out = reinterpret_cast<float*>(dst + ((size_t)e * R + r) * lut_entry_bytes(B));
+  if (lut_group(B) == 1) {
+    double sn, cs;
+    sincos((double)e * step, &sn, &cs);
+    out[0] = (float)cs;
+    out[1] = (float)sn;
+  } else {
+    const uint32_t M = (1u << B) - 1u;
+    double sa, ca, sb, cb;
+    sincos((double)(e & M) * step, &sa, &ca);
+    sincos((double)((e >> B) & M) * step, &sb, &cb);
+    out[0] = (float)ca;
+    out[1] = (float)cb;
+    out[2] = (float)sa;
+    out[3] = (float)sb;
+  }
+}
+
+// all (entry, copy) pairs of every tier's table, strided over `nthreads`
+__device__ inline void lut_fill(uint8_t* lut, const sphkv_tier_t* tiers, int n_tiers,
+                                const int* enc, int tid, int nthreads) {
+  for (int t = 1; t < n_tiers; ++t) {
+    if (enc[t] < 0) continue;
+    const int B = tiers[t].angle_bits;
+    const bool repl = enc[t] & 1;
+    const int R = repl ? lut_rep(B) : 1;
+    const int n = (1 << (lut_group(B) * B)) * R;
+    for (int i = tid; i < n; i += nthreads)
+      lut_write_entry(lut + (enc[t] >> 1), B, repl, i / R, i % R);
+  }
 }
 
 template <int B>
@@ -114,46 +173,37 @@ __device__ __forceinline__ void load_words(uint32_t (&w)[CodeWin<B>::WORDS],
 
 // One code row of the recurrence for the lane's 4 items (prod kept as two
 // packed pairs: items {0,1} and {2,3}).
-template <int B, int GP, bool LUT>
+template <int B, int GP, bool LUT, bool REPL>
 __device__ __forceinline__ void chain_row(const uint8_t* sm, const uint32_t (&w)[CodeWin<B>::WORDS],
                                           int sh, uint32_t qrow, uint32_t lut_s, float pstep,
                                           ptx::f2 (&prod)[2], ptx::f2 (&acc)[4][GP]) {
   ptx::f2 qv[GP];
   load_q<GP>(sm, qrow, qv);
   if constexpr (LUT && lut_group(B) > 1) {
-    constexpr int GS = lut_group(B);
-    ptx::f2 cp[2], sp[2];
-    if constexpr (B == 2) {
-      // the lane's 4 codes are one byte of the word: PRMT + LEA
-      const uint32_t idx = __byte_perm(w[0], 0u, 0x4440u | (uint32_t)(sh >> 3));
-      const uint32_t addr = lut_s + idx * 32u;
-      lds_pair2(sm, addr, cp[0], sp[0]);
-      lds_pair2(sm, addr + 16u, cp[1], sp[1]);
-    } else if constexpr (B == 4) {
+    // two pair lookups: items {0,1} and {2,3}; lut_s is this lane's copy base
+    constexpr uint32_t STRIDE = REPL ? 128u : 16u;
+    const uint32_t x = (uint32_t)code_window<B>(w, sh);
+    constexpr uint32_t M2 = (1u << (2 * B)) - 1u;
+    uint32_t i0, i1;
+    if constexpr (B == 4) {
       const uint32_t b0 = (uint32_t)(sh >> 3);
-      const uint32_t i0 = __byte_perm(w[0], 0u, 0x4440u | b0);
-      const uint32_t i1 = __byte_perm(w[0], 0u, 0x4440u | (b0 + 1));
-      lds_pair2(sm, lut_s + i0 * 16u, cp[0], sp[0]);
-      lds_pair2(sm, lut_s + i1 * 16u, cp[1], sp[1]);
-    } else if constexpr (GS == 4) {
-      const uint32_t x = (uint32_t)code_window<B>(w, sh);
-      const uint32_t addr = lut_s + (x & ((1u << (4 * B)) - 1u)) * 32u;
-      lds_pair2(sm, addr, cp[0], sp[0]);
-      lds_pair2(sm, addr + 16u, cp[1], sp[1]);
+      i0 = __byte_perm(w[0], 0u, 0x4440u | b0);
+      i1 = __byte_perm(w[0], 0u, 0x4440u | (b0 + 1));
     } else {
-      const uint32_t x = (uint32_t)code_window<B>(w, sh);
-      constexpr uint32_t M2 = (1u << (2 * B)) - 1u;
-      lds_pair2(sm, lut_s + (x & M2) * 16u, cp[0], sp[0]);
-      lds_pair2(sm, lut_s + ((x >> (2 * B)) & M2) * 16u, cp[1], sp[1]);
+      i0 = x & M2;
+      i1 = (x >> (2 * B)) & M2;
     }
+    ptx::f2 cp[2], sp[2];
+    lds_pair2(sm, lut_s + i0 * STRIDE, cp[0], sp[0]);
+    lds_pair2(sm, lut_s + i1 * STRIDE, cp[1], sp[1]);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const ptx::f2 f = ptx::f2_mul(prod[h], cp[h]);
-      prod[h] = ptx::f2_mul(prod[h], sp[h]);
+      ptx::f2_mul_acc(prod[h], sp[h]);
 #pragma unroll
       for (int g = 0; g < GP; ++g) {
-        acc[2 * h][g] = ptx::f2_fma_s(ptx::f2_lo(f), qv[g], acc[2 * h][g]);
-        acc[2 * h + 1][g] = ptx::f2_fma_s(ptx::f2_hi(f), qv[g], acc[2 * h + 1][g]);
+        ptx::f2_fma_s_acc(ptx::f2_lo(f), qv[g], acc[2 * h][g]);
+        ptx::f2_fma_s_acc(ptx::f2_hi(f), qv[g], acc[2 * h + 1][g]);
       }
     }
   } else {
@@ -165,7 +215,7 @@ __device__ __forceinline__ void chain_row(const uint8_t* sm, const uint32_t (&w)
       const uint32_t c = code_at<B>(y, k);
       float cs, sn;
       if constexpr (LUT) {
-        const float2 t = lds_f2(sm, lut_s + c * 8u);
+        const float2 t = lds_f2(sm, lut_s + c * (REPL ? 128u : 8u));
         cs = t.x;
         sn = t.y;
       } else {
@@ -173,7 +223,7 @@ __device__ __forceinline__ void chain_row(const uint8_t* sm, const uint32_t (&w)
       }
       const float f = pr[k] * cs;
 #pragma unroll
-      for (int g = 0; g < GP; ++g) acc[k][g] = ptx::f2_fma_s(f, qv[g], acc[k][g]);
+      for (int g = 0; g < GP; ++g) ptx::f2_fma_s_acc(f, qv[g], acc[k][g]);
       pr[k] *= sn;
     }
     prod[0] = ptx::f2_make(pr[0], pr[1]);
@@ -188,12 +238,13 @@ __device__ __forceinline__ void chain_row(const uint8_t* sm, const uint32_t (&w)
 // Code words are requested LA rows ahead of use through a ring of register
 // buffers (no moves of in-flight loads); the look-ahead may read a few rows
 // past the block, which the code pool's tail slack absorbs.
-template <int B, int GP, bool LUT>
-__device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes, int d, int P,
+template <int B, int GP, bool LUT, bool REPL, int PT>
+__device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes, int d, int P_rt,
                                                int TI, const sphkv_page_t& pg, int sub, int lane,
                                                const uint8_t* sm, uint32_t qs_s, uint32_t lut_s,
                                                float lg[4][2 * GP]) {
   constexpr int NW = CodeWin<B>::WORDS;
+  const int P = PT ? PT : P_rt;  // PT != 0: page size known at compile time (row stride immediates)
   const int item0 = sub * TI + 4 * lane;
   const uint32_t* base = reinterpret_cast<const uint32_t*>(codes + pg.code_off);
   const int row_words = P * B / 32;
@@ -214,7 +265,7 @@ __device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes
   // ring of LA+1 word buffers: row j+LA is requested while row j is consumed;
   // the unroll by LA+1 makes every buffer index a compile-time constant.
 #ifndef SPHKV_LA
-#define SPHKV_LA 4
+#define SPHKV_LA 6
 #endif
   constexpr int LA = SPHKV_LA;
   uint32_t wb[LA + 1][NW];
@@ -228,7 +279,7 @@ __device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes
 #pragma unroll
     for (int u = 0; u <= LA; ++u) {
       load_words<B>(wb[(u + LA) % (LA + 1)], next + u * row_words);  // may run past row d-1: pool has slack
-      chain_row<B, GP, LUT>(sm, wb[u], sh, qrow + u * qstride, lut_s, pstep, prod, acc);
+      chain_row<B, GP, LUT, REPL>(sm, wb[u], sh, qrow + u * qstride, lut_s, pstep, prod, acc);
     }
     next += (LA + 1) * row_words;
     qrow += (LA + 1) * qstride;
@@ -238,7 +289,7 @@ __device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes
   if (r == LA) load_words<B>(wb[LA], next);
 #pragma unroll
   for (int u = 0; u < LA; ++u)
-    if (u < r) chain_row<B, GP, LUT>(sm, wb[u], sh, qrow + u * qstride, lut_s, pstep, prod, acc);
+    if (u < r) chain_row<B, GP, LUT, REPL>(sm, wb[u], sh, qrow + u * qstride, lut_s, pstep, prod, acc);
   uint32_t w0[NW];
 #pragma unroll
   for (int u = 0; u <= LA; ++u) {
@@ -257,21 +308,21 @@ __device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes
   int j = 0;
   for (; j + 3 <= nrow; j += 3) {
     load_words<B>(w2, next);
-    chain_row<B, GP, LUT>(sm, w0, sh, qrow, lut_s, pstep, prod, acc);
+    chain_row<B, GP, LUT, REPL>(sm, w0, sh, qrow, lut_s, pstep, prod, acc);
     load_words<B>(w0, next + row_words);
-    chain_row<B, GP, LUT>(sm, w1, sh, qrow + qstride, lut_s, pstep, prod, acc);
+    chain_row<B, GP, LUT, REPL>(sm, w1, sh, qrow + qstride, lut_s, pstep, prod, acc);
     load_words<B>(w1, next + 2 * row_words);
-    chain_row<B, GP, LUT>(sm, w2, sh, qrow + 2 * qstride, lut_s, pstep, prod, acc);
+    chain_row<B, GP, LUT, REPL>(sm, w2, sh, qrow + 2 * qstride, lut_s, pstep, prod, acc);
     next += 3 * row_words;
     qrow += 3 * qstride;
   }
   const int rem = nrow - j;
   if (rem >= 1) {
-    chain_row<B, GP, LUT>(sm, w0, sh, qrow, lut_s, pstep, prod, acc);
+    chain_row<B, GP, LUT, REPL>(sm, w0, sh, qrow, lut_s, pstep, prod, acc);
     qrow += qstride;
     if (rem == 2) {
       load_words<B>(w2, next);
-      chain_row<B, GP, LUT>(sm, w1, sh, qrow, lut_s, pstep, prod, acc);
+      chain_row<B, GP, LUT, REPL>(sm, w1, sh, qrow, lut_s, pstep, prod, acc);
 #pragma unroll
       for (int i = 0; i < NW; ++i) w0[i] = w2[i];
     } else {
@@ -319,21 +370,35 @@ __device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes
 template <int GP>
 __device__ void ada_logit_dispatch(int B, const uint8_t* codes, int d, int P, int TI,
                                    const sphkv_page_t& pg, int sub, int lane, const uint8_t* sm,
-                                   uint32_t qs_s, uint32_t lut_s, bool has_lut,
-                                   float lg[4][2 * GP]) {
+                                   uint32_t qs_s, int lut_enc, float lg[4][2 * GP]) {
+  // lut_enc: (byte offset << 1) | replicated, or -1 (no table: sincospi)
+  const bool has = lut_enc >= 0;
+  const bool repl = has && (lut_enc & 1);
+  const uint32_t base = has ? (uint32_t)(lut_enc >> 1) : 0u;
   switch (B) {
-#define SPHKV_CASE(b)                                                                    \
-  case b:                                                                                \
-    if (b <= LUT_MAX_BITS && has_lut)                                                    \
-      ada_logit_tile<b, GP, (b <= LUT_MAX_BITS)>(codes, d, P, TI, pg, sub, lane, sm,     \
-                                                 qs_s, lut_s, lg);                       \
-    else                                                                                 \
-      ada_logit_tile<b, GP, false>(codes, d, P, TI, pg, sub, lane, sm, qs_s, lut_s, lg); \
+#define SPHKV_TILE(b, L, R, PP)                                                              \
+  ada_logit_tile<b, GP, L, R, PP>(codes, d, P, TI, pg, sub, lane, sm, qs_s,                 \
+                                  base + (R ? (uint32_t)(lane % lut_rep(b)) * lut_entry_bytes(b) \
+                                            : 0u), lg)
+#define SPHKV_CASE(b)                                                                        \
+  case b:                                                                                    \
+    if (b <= LUT_MAX_BITS && has) {                                                          \
+      if (repl) {                                                                            \
+        if (P == 256) SPHKV_TILE(b, (b <= LUT_MAX_BITS), true, 256);                         \
+        else SPHKV_TILE(b, (b <= LUT_MAX_BITS), true, 0);                                    \
+      } else {                                                                               \
+        if (P == 256) SPHKV_TILE(b, (b <= LUT_MAX_BITS), false, 256);                        \
+        else SPHKV_TILE(b, (b <= LUT_MAX_BITS), false, 0);                                   \
+      }                                                                                      \
+    } else {                                                                                 \
+      SPHKV_TILE(b, false, false, 0);                                                        \
+    }                                                                                        \
     break;
     SPHKV_CASE(1) SPHKV_CASE(2) SPHKV_CASE(3) SPHKV_CASE(4) SPHKV_CASE(5) SPHKV_CASE(6)
     SPHKV_CASE(7) SPHKV_CASE(8) SPHKV_CASE(9) SPHKV_CASE(10) SPHKV_CASE(11) SPHKV_CASE(12)
     SPHKV_CASE(13) SPHKV_CASE(14) SPHKV_CASE(15) SPHKV_CASE(16)
 #undef SPHKV_CASE
+#undef SPHKV_TILE
     default: break;
   }
 }

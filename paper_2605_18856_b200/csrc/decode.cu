@@ -27,12 +27,26 @@
 namespace sphkv {
 
 constexpr float kLog2e = 1.4426950408889634f;
-constexpr int ADA_NL = 7;          // logit warps
+#ifndef SPHKV_NL
+#define SPHKV_NL 7
+#endif
+constexpr int ADA_NL = SPHKV_NL;   // logit warps
 constexpr int ADA_TI = 128;        // items per tile (4 per lane)
-constexpr int ADA_NS = 16;         // P slots
-constexpr int ADA_NV = 4;          // V slots
-constexpr int ADA_THREADS = (ADA_NL + 1) * 32;  // 8 warps -> up to 255 registers
-constexpr int MAX_UNIT_TILES = 1024;
+constexpr int ADA_NS = 12;         // P slots
+constexpr int ADA_NV = 3;          // V slots
+#ifndef SPHKV_PF_MODE
+#define SPHKV_PF_MODE 0
+#endif
+#ifndef SPHKV_PF_ROUNDS
+#define SPHKV_PF_ROUNDS 2
+#endif
+#ifndef SPHKV_NPV
+#define SPHKV_NPV 1
+#endif
+constexpr int ADA_NPV = SPHKV_NPV;  // PV warps (split d_v)
+constexpr int ADA_MTW = 8 / ADA_NPV; // m-tiles per PV warp (d_v <= 128)
+constexpr int ADA_THREADS = (ADA_NL + ADA_NPV) * 32;
+constexpr int MAX_UNIT_TILES = 512;
 constexpr int PROW_PAD = 16;       // bytes of padding per P row (bank spread)
 
 struct AdaParams {
@@ -44,9 +58,9 @@ struct AdaParams {
   float* partials;
   float* logits_dbg;
   const int64_t* dbg_off;
-  int lut_off[SPHKV_MAX_TIERS];   // float2 offset of each tier's polar LUT, -1 = none
-  int lut_entries;
-  const float2* lut_global;       // prebuilt tables (sphkv_store_build_lut) or NULL
+  int lut_off[SPHKV_MAX_TIERS];   // encoded table descriptor per tier (see lut_layout_tiers)
+  int lut_bytes;                  // LUT region size
+  const uint8_t* lut_global;      // prebuilt tables (sphkv_store_build_lut) or NULL
   int TI;                   // tile items (min(P, 128))
   int dvp;                  // d_v padded to 16
   uint32_t smem_q, smem_tiles, smem_p, smem_v, smem_bar;  // byte offsets
@@ -146,26 +160,32 @@ __device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int T
   }
 }
 
+// Online-softmax state of one PV warp for its m-tiles [mt0, mt0 + MTW) of d_v.
+template <int MTW>
 struct PVState {
-  float acc[8][4];
+  float acc[MTW][4];
   float m[2], l[2];
 };
 
-__device__ __forceinline__ void pv_init(PVState& s) {
+template <int MTW>
+__device__ __forceinline__ void pv_init(PVState<MTW>& s) {
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MTW; ++i)
 #pragma unroll
     for (int r = 0; r < 4; ++r) s.acc[i][r] = 0.f;
   s.m[0] = s.m[1] = -INFINITY;
   s.l[0] = s.l[1] = 0.f;
 }
 
-// One tile of P.V on mma.sync + online combine.
-__device__ __forceinline__ void pv_tile(PVState& s, const uint8_t* pslot, const uint8_t* vslot,
-                                        int prow_bytes, int TI, int dvp, int MT, int G, int lane) {
-  float c[8][4];
+// One tile of P.V on mma.sync (A = V^T from the swizzled smem tile via
+// ldmatrix.trans, B = fp16 weights of the P slot) + online combine.
+template <int MTW>
+__device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, const uint8_t* vslot,
+                                        int prow_bytes, int TI, int dvp, int mt0, int mtn, int G,
+                                        int lane) {
+  float c[MTW][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MTW; ++i)
 #pragma unroll
     for (int r = 0; r < 4; ++r) c[i][r] = 0.f;
   const int nchunks = dvp / 8;
@@ -178,52 +198,53 @@ __device__ __forceinline__ void pv_tile(PVState& s, const uint8_t* pslot, const 
     ptx::ldsm_x2(pbase + (lane & 7) * prow_bytes + (ks * 16 + ((lane >> 3) & 1) * 8) * 2, b0, b1);
     const int item = ks * 16 + r + (mat >> 1) * 8;
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      if (mt < MT) {
-        int chunk = 2 * mt + (mat & 1);
-        int sw = chunk ^ (r & smask);
+    for (int i = 0; i < MTW; ++i) {
+      if (i < mtn) {
+        const int chunk = 2 * (mt0 + i) + (mat & 1);
+        const int sw = chunk ^ (r & smask);
         uint32_t a0, a1, a2, a3;
         ptx::ldsm_x4_trans(vbase + (item * dvp + sw * 8) * 2, a0, a1, a2, a3);
-        ptx::mma_f16(c[mt], a0, a1, a2, a3, b0, b1);
+        ptx::mma_f16(c[i], a0, a1, a2, a3, b0, b1);
       }
     }
   }
   const float* hdr = reinterpret_cast<const float*>(pslot + 8 * prow_bytes);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    int g = 2 * (lane & 3) + h;
-    float mt_ = (g < G) ? hdr[g] : 0.f;
-    float lt = (g < G) ? hdr[8 + g] : 0.f;
-    float mn = fmaxf(s.m[h], mt_);
-    float al = exp2f(s.m[h] - mn), be = exp2f(mt_ - mn);
+    const int g = 2 * (lane & 3) + h;
+    const float mt_ = (g < G) ? hdr[g] : 0.f;
+    const float lt = (g < G) ? hdr[8 + g] : 0.f;
+    const float mn = fmaxf(s.m[h], mt_);
+    const float al = exp2f(s.m[h] - mn), be = exp2f(mt_ - mn);
     s.m[h] = mn;
     s.l[h] = s.l[h] * al + lt * be;
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      s.acc[mt][h] = s.acc[mt][h] * al + c[mt][h] * be;
-      s.acc[mt][2 + h] = s.acc[mt][2 + h] * al + c[mt][2 + h] * be;
+    for (int i = 0; i < MTW; ++i) {
+      s.acc[i][h] = s.acc[i][h] * al + c[i][h] * be;
+      s.acc[i][2 + h] = s.acc[i][2 + h] * al + c[i][2 + h] * be;
     }
   }
 }
 
-__device__ __forceinline__ void pv_write(const PVState& s, float* part, int G, int d_v, int MT,
-                                         int lane) {
-  // layout: m[G], l[G], acc[G][d_v]
+// Partial layout per slot: m[G], l[G], acc[G][d_v] (base-2 logit units).
+template <int MTW>
+__device__ __forceinline__ void pv_write(const PVState<MTW>& s, float* part, int G, int d_v,
+                                         int mt0, int mtn, bool write_ml, int lane) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    int g = 2 * (lane & 3) + h;
+    const int g = 2 * (lane & 3) + h;
     if (g >= G) continue;
-    if ((lane >> 2) == 0) {
+    if (write_ml && (lane >> 2) == 0) {
       part[g] = s.m[h];
       part[G + g] = s.l[h];
     }
     float* a = part + 2 * G + (size_t)g * d_v;
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      if (mt >= MT) continue;
-      int r0 = mt * 16 + (lane >> 2);
-      if (r0 < d_v) a[r0] = s.acc[mt][h];
-      if (r0 + 8 < d_v) a[r0 + 8] = s.acc[mt][2 + h];
+    for (int i = 0; i < MTW; ++i) {
+      if (i >= mtn) continue;
+      const int r0 = (mt0 + i) * 16 + (lane >> 2);
+      if (r0 < d_v) a[r0] = s.acc[i][h];
+      if (r0 + 8 < d_v) a[r0 + 8] = s.acc[i][2 + h];
     }
   }
 }
@@ -240,6 +261,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   float2* qs = reinterpret_cast<float2*>(smem + p.smem_q);
   TileEntry* tiles = reinterpret_cast<TileEntry*>(smem + p.smem_tiles);
   int* ntiles_s = reinterpret_cast<int*>(smem + p.smem_tiles + MAX_UNIT_TILES * sizeof(TileEntry));
+  int* tile_ctr = ntiles_s + 1;
   uint8_t* pslots = smem + p.smem_p;
   uint8_t* vslots = smem + p.smem_v;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
@@ -252,24 +274,20 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 
   // polar LUTs (fp64 sincos rounded to fp32), barrier init
   if (p.lut_global != nullptr) {
-    const float4* src = reinterpret_cast<const float4*>(p.lut_global);
-    float4* dst = reinterpret_cast<float4*>(lut);
-    for (int i = threadIdx.x; i < (p.lut_entries + 1) / 2; i += blockDim.x) dst[i] = __ldg(src + i);
-  } else
-  for (int t = 0; t < st.n_tiers; ++t) {
-    int off = p.lut_off[t];
-    if (off < 0) continue;
-    int b = st.tiers[t].angle_bits;
-    for (int i = threadIdx.x; i < lut_float2s(b); i += blockDim.x) lut[off + i] = lut_slot(b, i);
+    const uint4* src = reinterpret_cast<const uint4*>(p.lut_global);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    for (int i = threadIdx.x; i < p.lut_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+  } else {
+    lut_fill(smem, st.tiers, st.n_tiers, p.lut_off, threadIdx.x, blockDim.x);
   }
   if (threadIdx.x == 0) {
     for (int i = 0; i < ADA_NS; ++i) {
       ptx::mbar_init(&p_full[i], 1);
-      ptx::mbar_init(&p_empty[i], 1);
+      ptx::mbar_init(&p_empty[i], ADA_NPV);
     }
     for (int i = 0; i < ADA_NV; ++i) {
       ptx::mbar_init(&v_full[i], 1);
-      ptx::mbar_init(&v_empty[i], 1);
+      ptx::mbar_init(&v_empty[i], ADA_NPV);
     }
   }
   __syncthreads();
@@ -278,7 +296,10 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   uint32_t gbase = 0;  // running tile sequence number (barrier phases)
   for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
     const sphkv_unit_t unit = p.units[u];
-    if (warp == 0) build_tiles(st, unit, TI, tiles, ntiles_s, lane);
+    if (warp == 0) {
+      build_tiles(st, unit, TI, tiles, ntiles_s, lane);
+      if (lane == 0) *tile_ctr = 0;
+    }
     // q rows for this group, prescaled into base-2 logit units, packed pairs
     const float* qg = p.q + (size_t)unit.group * p.G * d;
     for (int i = threadIdx.x; i < d * GP; i += blockDim.x) {
@@ -292,33 +313,53 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 
     if (warp < ADA_NL) {
       // ---------------- logit warps ----------------
-      for (int k = warp; k < nt; k += ADA_NL) {
+      // tiles are claimed dynamically (smem counter) to balance the warps;
+      // the P slot of tile k is k % NS whoever computes it.
+      const uint64_t ppol = ptx::policy_evict_last();
+      // L2 prefetch of a page's code block (one per page, at its sub-0 tile):
+      // SPHKV_PF_MODE 0 = one bulk prefetch by lane 0, 1 = per-line prefetch by
+      // the whole warp (evict_last either way)
+      auto prefetch_tile = [&](int t) {
+        if (t < nt) {
+          const TileEntry tn = tiles[t];
+          if ((tn.sub_off >> 24) == 0) {
+            const sphkv_page_t pn = st.pages[tn.page];
+            const uint32_t bytes = (uint32_t)code_block_bytes(d, P, pn.abits, pn.rbits);
+#if SPHKV_PF_MODE == 0
+            if (lane == 0) ptx::bulk_prefetch_l2_hint(st.codes + pn.code_off, bytes, ppol);
+#else
+            for (uint32_t o = lane * 128u; o < bytes; o += 32u * 128u)
+              ptx::prefetch_l2_line(st.codes + pn.code_off + o);
+#endif
+          }
+        }
+      };
+#pragma unroll 1
+      for (int r = 0; r < SPHKV_PF_ROUNDS; ++r) prefetch_tile(warp + r * ADA_NL);
+      for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(tile_ctr, 1);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= nt) break;
+        prefetch_tile(k + SPHKV_PF_ROUNDS * ADA_NL);
         const uint32_t gk = gbase + k;
         const TileEntry te = tiles[k];
         const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
         const sphkv_page_t pg = st.pages[te.page];
-        // prefetch my next tile's code block into L2
-        if (k + ADA_NL < nt && lane == 0) {
-          const TileEntry tn = tiles[k + ADA_NL];
-          if ((tn.sub_off >> 24) == 0) {
-            const sphkv_page_t pn = st.pages[tn.page];
-            uint32_t bytes = (uint32_t)code_block_bytes(d, P, pn.abits, pn.rbits);
-            ptx::bulk_prefetch_l2_hint(st.codes + pn.code_off, bytes, ptx::policy_evict_last());
-          }
-        }
         const int ti = tier_index(st, pg.tier);
-        const int loff = p.lut_off[ti];
-        const uint32_t lut_s = (loff >= 0 ? loff : 0) * 8u;  // LUT region starts at smem[0]
-        float lg[4][2 * GP];
+        float lg[4][2 * GP];  // LUT region starts at smem[0]
         ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, TI, pg, sub, lane, smem, p.smem_q,
-                               lut_s, loff >= 0, lg);
+                               p.lut_off[ti], lg);
         int nvalid = pg.count - sub * TI - 4 * lane;
         nvalid = nvalid < 0 ? 0 : (nvalid > 4 ? 4 : nvalid);
         if (4 * lane >= TI) nvalid = 0;
         if (p.logits_dbg != nullptr) {
           float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 4 * lane) * p.G;
-          for (int kk = 0; kk < nvalid; ++kk)
-            for (int g = 0; g < p.G; ++g) dst[kk * p.G + g] = lg[kk][g] * (1.0f / kLog2e);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int g = 0; g < 2 * GP; ++g)
+              if (kk < nvalid && g < p.G) dst[kk * p.G + g] = lg[kk][g] * (1.0f / kLog2e);
         }
         const int ps = gk % ADA_NS;
         ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
@@ -327,37 +368,46 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
       }
     } else {
-      // ---------------- PV warp (also the V producer) ----------------
+      // ---------------- PV warps ----------------
+      // NPV warps split the d_v m-tiles; all consume every tile in order.
+      // Lane 0 of PV warp 0 is also the V producer: it refills slot vs once
+      // every PV warp has released it (v_empty counts NPV arrivals).
+      const int pw = warp - ADA_NL;
+      const int mtw = (MT + ADA_NPV - 1) / ADA_NPV;
+      const int mt0 = pw * mtw;
+      const int mtn = max(0, min(mtw, MT - mt0));
       const uint64_t vpol = ptx::policy_evict_first();
       auto issue_v = [&](int k) {
         const uint32_t gk = gbase + k;
         const int vs = gk % ADA_NV;
+        ptx::mbar_wait(&v_empty[vs], ((gk / ADA_NV) & 1) ^ 1);
         const TileEntry te = tiles[k];
         const int sub = te.sub_off >> 24;
         const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)sub * TI) * dvp;
-        ptx::fence_proxy_async();  // order this warp's earlier ldmatrix reads of the slot
+        ptx::fence_proxy_async();  // order earlier ldmatrix reads of the slot
         ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
         ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
       };
-      if (lane == 0)
+      if (pw == 0 && lane == 0)
         for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k);
-      PVState s;
+      PVState<ADA_MTW> s;
       pv_init(s);
       for (int k = 0; k < nt; ++k) {
         const uint32_t gk = gbase + k;
         const int vs = gk % ADA_NV, ps = gk % ADA_NS;
         ptx::mbar_wait(&v_full[vs], (gk / ADA_NV) & 1);
         ptx::mbar_wait(&p_full[ps], (gk / ADA_NS) & 1);
-        pv_tile(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes, p.prow_bytes, TI,
-                dvp, MT, p.G, lane);
+        pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                         p.prow_bytes, TI, dvp, mt0, mtn, p.G, lane);
         __syncwarp();
         if (lane == 0) {
           ptx::mbar_arrive(&p_empty[ps]);
-          if (k + ADA_NV < nt) issue_v(k + ADA_NV);  // slot vs is free again
+          ptx::mbar_arrive(&v_empty[vs]);
+          if (pw == 0 && k + ADA_NV < nt) issue_v(k + ADA_NV);
         }
       }
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
-      pv_write(s, part, p.G, st.d_v, MT, lane);
+      pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane);
     }
     gbase += nt;
     __syncthreads();
@@ -506,15 +556,15 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
         if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
       }
     } else if (warp == DN_NL) {
-      PVState s;
+      PVState<8> s;
       pv_init(s);
       for (int k = 0; k < nt; ++k) {
         const uint32_t gk = gbase + k;
         const int vs = gk % DN_NV, ps = gk % DN_NS;
         ptx::mbar_wait(&v_full[vs], (gk / DN_NV) & 1);
         ptx::mbar_wait(&p_full[ps], (gk / DN_NS) & 1);
-        pv_tile(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes, p.prow_bytes, DN_TI,
-                dvp, MT, p.G, lane);
+        pv_tile<8>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes, p.prow_bytes,
+                   DN_TI, dvp, 0, MT, p.G, lane);
         __syncwarp();
         if (lane == 0) {
           ptx::mbar_arrive(&p_empty[ps]);
@@ -522,7 +572,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
         }
       }
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
-      pv_write(s, part, p.G, st.d_v, MT, lane);
+      pv_write<8>(s, part, p.G, st.d_v, 0, MT, true, lane);
     } else if (lane == 0) {
       for (int k = 0; k < nt; ++k) {
         const uint32_t gk = gbase + k;
@@ -580,45 +630,27 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 extern "C" int64_t sphkv_partial_floats(int G, int d_v) { return (int64_t)G * (d_v + 2); }
 
-// narrowest tiers first until the shared-memory budget is used
 static int lut_layout(const sphkv_store_t* st, int off[SPHKV_MAX_TIERS]) {
-  int used = 0;
-  for (int t = 0; t < SPHKV_MAX_TIERS; ++t) off[t] = -1;
-  for (int pass_b = 1; pass_b <= LUT_MAX_BITS; ++pass_b)
-    for (int t = 1; t < st->n_tiers; ++t)
-      if (st->tiers[t].angle_bits == pass_b && used + lut_float2s(pass_b) <= LUT_BUDGET) {
-        off[t] = used;  // every table size is even -> 16-B aligned offsets
-        used += lut_float2s(pass_b);
-      }
-  return used;
+  return lut_layout_tiers(st->tiers, st->n_tiers, off);
 }
 
 namespace sphkv {
-__global__ void k_build_lut(sphkv_store_t st, int entries) {
-  for (int t = 0; t < st.n_tiers; ++t) {
-    int off = st.lut_off[t];
-    if (off < 0) continue;
-    int b = st.tiers[t].angle_bits;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < lut_float2s(b);
-         i += gridDim.x * blockDim.x) {
-      const float2 v = lut_slot(b, i);
-      st.lut[2 * (off + i)] = v.x;
-      st.lut[2 * (off + i) + 1] = v.y;
-    }
-  }
+__global__ void k_build_lut(sphkv_store_t st) {
+  lut_fill(reinterpret_cast<uint8_t*>(st.lut), st.tiers, st.n_tiers, st.lut_off,
+           blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
 }
 }  // namespace sphkv
 
 extern "C" int64_t sphkv_lut_floats(const sphkv_store_t* st) {
   int off[SPHKV_MAX_TIERS];
-  return 2 * (int64_t)lut_layout(st, off) + 4;
+  return lut_layout(st, off) / 4 + 4;
 }
 
 extern "C" int sphkv_store_build_lut(sphkv_store_t* st, cudaStream_t stream) {
   if (!st || !st->lut) return fail(SPHKV_E_VALUE, "store lut buffer missing");
   int used = lut_layout(st, st->lut_off);
   if (used == 0) return SPHKV_OK;
-  k_build_lut<<<16, 256, 0, stream>>>(*st, used);
+  k_build_lut<<<64, 256, 0, stream>>>(*st);
   SPHKV_LAUNCH_CHECK();
   return SPHKV_OK;
 }
@@ -662,15 +694,15 @@ extern "C" int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
   p.TI = st->page_size < ADA_TI ? st->page_size : ADA_TI;
   p.dvp = (st->d_v + 15) / 16 * 16;
   int used = lut_layout(st, p.lut_off);
-  p.lut_entries = used;
+  p.lut_bytes = used;
   p.lut_global = nullptr;
   if (st->lut != nullptr) {
     bool same = true;
     for (int t = 0; t < SPHKV_MAX_TIERS; ++t) same = same && (st->lut_off[t] == p.lut_off[t]);
-    if (same) p.lut_global = reinterpret_cast<const float2*>(st->lut);
+    if (same) p.lut_global = reinterpret_cast<const uint8_t*>(st->lut);
   }
   const int GP = (G + 1) / 2;
-  size_t off = align_up((size_t)used * 8, 128);
+  size_t off = align_up((size_t)used, 128);
   p.smem_q = (uint32_t)off;
   off = align_up(off + (size_t)st->d * GP * 8, 128);
   p.smem_tiles = (uint32_t)off;

@@ -82,6 +82,9 @@ __device__ __forceinline__ void bulk_prefetch_l2_hint(const void* src, uint32_t 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2_line(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -140,6 +143,15 @@ __device__ __forceinline__ f2 f2_fma_s(float s, f2 q, f2 acc) {
   f2 ss = f2_make(s, s);
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(ss.v), "l"(q.v), "l"(acc.v));
   return r;
+}
+// in-place accumulate (tied operand): keeps loop-carried accumulators in
+// fixed registers so unrolled loops need no copy-back moves
+__device__ __forceinline__ void f2_fma_s_acc(float s, f2 q, f2& acc) {
+  f2 ss = f2_make(s, s);
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc.v) : "l"(ss.v), "l"(q.v));
+}
+__device__ __forceinline__ void f2_mul_acc(f2& a, f2 b) {
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(a.v) : "l"(b.v));
 }
 
 __device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {

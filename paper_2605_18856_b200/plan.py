@@ -19,7 +19,7 @@ import numpy as np
 from . import _lib
 
 SM_COUNT = 148
-MAX_UNIT_TILES = 1024
+MAX_UNIT_TILES = 512
 TILE_ITEMS = 128
 PAGE_HEADER_BYTES = 16
 
