@@ -186,7 +186,9 @@ def build_workload(cfg_name, rank=0, seed=0):
     ds.bulk_load(wl.keys, wl.values)
     torch.cuda.synchronize()
     tim["dense_fill_ms"] = (time.time() - t0) * 1e3
-    info = {"budget_frac_of_dense_key_bits": best_frac, "resident_ada": int(res),
+    hist = torch.bincount(tier.view(-1).long(), minlength=8).cpu().tolist()
+    info = {"tier_items": {str(t.id): int(hist[t.id]) for t in tiers.tiers},
+            "budget_frac_of_dense_key_bits": best_frac, "resident_ada": int(res),
             "resident_dense": int(dense_res), "resident_ratio": res / dense_res}
     return dict(wl=wl, st=st, ds=ds, tiers=tiers, radii=radii, z=z, tier=tier, info=info,
                 timings=tim, u_hat=u_hat, s_hat=s_hat, r_q=r_q)
@@ -262,12 +264,16 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no graphs (for ncu)")
     ap.add_argument("--units-per-cta", type=int, default=1)
+    ap.add_argument("--unfused", action="store_true",
+                    help="separate LSE-merge launch per layer (default: merge fused in the decode)")
+    ap.add_argument("--dynamic", action="store_true",
+                    help="CTAs claim units from a global queue (longest first)")
     ap.add_argument("--fuse-layers", action="store_true",
                     help="one decode launch over all layers (attention-only benchmark shortcut)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))  # N > 1 only under torchrun
     local = int(os.environ.get("LOCAL_RANK", "0"))
     B, L, H, G, T, d, desc = CONFIGS[args.config]
     metric = "ADA decode tokens/s at 128K ctx, achieved HBM GB/s vs peak, KV bytes/token"
@@ -276,7 +282,7 @@ def main():
               "l2": "inputs larger than L2 (no flush needed)", "batch": B, "layers": L,
               "kv_heads": H, "q_heads": H * G, "tokens": T, "d": d,
               "parallelism": f"page-range split x{world}" if world > 1 else "single GPU",
-              "launch": "one decode+merge per layer (CUDA graph)"}
+              "launch": "one decode launch per layer, split merge fused in-kernel (CUDA graph)"}
 
     import torch
 
@@ -324,8 +330,9 @@ def main():
 
     def ada_plan(s, groups):
         if world == 1:
-            return planmod.plan_store(s, groups=groups, units_per_cta=args.units_per_cta)
-        return planmod.plan_store_range(s, groups, rank, world)
+            return planmod.plan_store(s, groups=groups, units_per_cta=args.units_per_cta,
+                                      dynamic=args.dynamic)
+        return planmod.plan_store_range(s, groups, rank, world, units_per_cta=args.units_per_cta)
 
     if args.fuse_layers:
         plans = [ada_plan(st, list(range(B * L * H)))]
@@ -333,7 +340,8 @@ def main():
     else:
         plans = layer_plans(st, L, H, B, rank, world, ada_plan)
     n_launch = len(plans)
-    dplans = [planmod.plan_dense(ds, groups=[(b * L + l) * H + h for b in range(B) for h in range(H)])
+    dplans = [planmod.plan_dense(ds, groups=[(b * L + l) * H + h for b in range(B) for h in range(H)],
+                                 dynamic=args.dynamic)
               for l in range(L)] if not args.no_dense else []
     q = wl.queries
     outs = [torch.empty((len(p.group_ids) * G, d), dtype=torch.float32, device="cuda") for p in plans]
@@ -342,8 +350,16 @@ def main():
     stream = torch.cuda.Stream()
     sp = stream.cuda_stream
 
+    fused = world == 1 and not args.unfused
+
     def decode_layers(with_merge=True):
         for l, p in enumerate(plans):
+            if fused:
+                _lib.check(lib.sphkv_ada_decode_fused(
+                    st.cptr, q.data_ptr(), G, p.units.data_ptr(), p.n_units, parts[l].data_ptr(),
+                    p.slot_group.data_ptr(), p.slot_begin.data_ptr(), len(p.group_ids),
+                    p.ctl.data_ptr(), outs[l].data_ptr(), int(p.dynamic), p.grid, sp))
+                continue
             _lib.check(lib.sphkv_ada_decode(st.cptr, q.data_ptr(), G, p.units.data_ptr(),
                                             p.n_units, parts[l].data_ptr(), None, None, p.grid, sp))
             if with_merge and world == 1:
@@ -360,6 +376,12 @@ def main():
 
     def dense_layers():
         for l, p in enumerate(dplans):
+            if fused:
+                _lib.check(lib.sphkv_dense_decode_fused(
+                    ds.cptr, q.data_ptr(), G, p.units.data_ptr(), p.n_units, dparts[l].data_ptr(),
+                    p.slot_group.data_ptr(), p.slot_begin.data_ptr(), len(p.group_ids),
+                    p.ctl.data_ptr(), douts[l].data_ptr(), int(p.dynamic), p.grid, sp))
+                continue
             _lib.check(lib.sphkv_dense_decode(ds.cptr, q.data_ptr(), G, p.units.data_ptr(),
                                               p.n_units, dparts[l].data_ptr(), p.grid, sp))
             _lib.check(lib.sphkv_lse_merge(dparts[l].data_ptr(), p.slot_begin.data_ptr(),
@@ -377,17 +399,26 @@ def main():
 
     step_fn = decode_layers
     if world > 1:
+        # page-range split of every (seq, layer, kv-head) list: per layer the
+        # local splits are LSE-merged into one partial state per (group, q-head);
+        # the states of all layers go out in ONE all-gather per step (valid in
+        # this attention-only benchmark, where every layer's query is given),
+        # then one merge over ranks yields every layer's output on every rank.
         import torch.distributed as dist
 
-        gathered = [torch.empty(p.n_slots_total_floats, dtype=torch.float32, device="cuda")
-                    for p in plans]
+        ng = len(plans[0].group_ids)
+        F = G * (d + 2)
+        state = torch.empty((n_launch, ng, F), dtype=torch.float32, device="cuda")
+        gathered = torch.empty((world, n_launch, ng, F), dtype=torch.float32, device="cuda")
+        out_all = torch.empty((n_launch * ng * G, d), dtype=torch.float32, device="cuda")
 
         def step_fn():
             decode_layers(with_merge=False)
+            for l, p in enumerate(plans):
+                planmod.merge_local_state(p, parts[l], G, d, state[l], stream)
             with torch.cuda.stream(stream):
-                for l, p in enumerate(plans):
-                    dist.all_gather_into_tensor(gathered[l], parts[l][: p.local_floats])
-                    planmod.merge_gathered(p, gathered[l], G, d, outs[l], stream)
+                dist.all_gather_into_tensor(gathered.view(-1), state.view(-1))
+            planmod.merge_gathered(n_launch * ng, world, gathered, G, d, out_all, stream)
 
     # warmup + graph capture of the step (launch-bound loop of 64 kernels)
     with torch.cuda.stream(stream):
@@ -427,6 +458,7 @@ def main():
     # kernel-level timing of the dominant kernel (ADA decode, all layers)
     with torch.cuda.stream(stream):
         dec_ms = time_events(lambda: decode_layers(with_merge=False), max(args.steps // 2, 3)) / n_launch
+        # (fused: the per-launch time includes the in-kernel split merge)
     bytes_total = st.stream_bytes_total()
     qbytes = B * L * H * G * d * 4
     part_bytes = sum(p.n_slots for p in plans) * G * (d + 2) * 4
@@ -463,8 +495,11 @@ def main():
     def e2e_step():
         q.copy_(qh, non_blocking=True)
         run()
-        torch.cat(outs, out=ocat)
-        oh.copy_(ocat, non_blocking=True)
+        if world > 1:
+            oh.copy_(out_all, non_blocking=True)
+        else:
+            torch.cat(outs, out=ocat)
+            oh.copy_(ocat, non_blocking=True)
 
     with torch.cuda.stream(stream):
         for _ in range(2):
@@ -509,7 +544,8 @@ def main():
                 "e2e": {"value": B / (e2e_ms * 1e-3), "unit": "tokens/s",
                         "h2d_bytes_per_step": int(qh.numel() * 4),
                         "d2h_bytes_per_step": int(oh.numel() * 4)},
-                "gpu_launches": args.steps * (2 * n_launch if world == 1 else n_launch),
+                "gpu_launches": args.steps * (n_launch if fused else 2 * n_launch if world == 1
+                                              else 2 * n_launch + 1),
                 "clocks": clk, "prefill": W["timings"], "budget": W["info"]}
         print(json.dumps(line), flush=True)
     if world > 1:

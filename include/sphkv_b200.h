@@ -243,15 +243,47 @@ int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
                      float* logits_dbg, const int64_t* dbg_offsets, int grid,
                      cudaStream_t stream);
 
+/* ADA decode with the split merge fused in: the CTA that finishes the last
+ * split of a plan group merges that group's partial slots into `out` fp32
+ * [n_groups*G, d_v] (same result as sphkv_lse_merge).  slot_group int32
+ * [n_slots] gives each partial slot's plan group (-1 = scratch slot);
+ * slot_begin as for sphkv_lse_merge; ctl int32 [n_groups + 2] must be zero
+ * before the first call and is left zero (CUDA-graph replay safe).
+ * dynamic != 0: CTAs claim units from a global queue in list order (plan the
+ * list longest-first) instead of the static u += grid assignment. */
+int sphkv_ada_decode_fused(const sphkv_store_t* st, const float* q, int G,
+                           const sphkv_unit_t* units, int n_units, float* partials,
+                           const int32_t* slot_group, const int32_t* slot_begin, int n_groups,
+                           int32_t* ctl, float* out, int dynamic, int grid,
+                           cudaStream_t stream);
+
 /* Dense bf16 paged decode with the same unit/partial contract. */
 int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,
                        const sphkv_unit_t* units, int n_units, float* partials,
                        int grid, cudaStream_t stream);
 
+/* Dense decode with the fused split merge / dynamic queue (as above). */
+int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const float* q, int G,
+                             const sphkv_unit_t* units, int n_units, float* partials,
+                             const int32_t* slot_group, const int32_t* slot_begin,
+                             int n_groups, int32_t* ctl, float* out, int dynamic, int grid,
+                             cudaStream_t stream);
+
 /* Split-context LSE merge: out fp32 [n_groups*G, d_v]; group g's partials
  * are slots [slot_begin[g], slot_begin[g+1]). Empty splits carry m = -inf. */
 int sphkv_lse_merge(const float* partials, const int32_t* slot_begin,
                     int n_groups, int G, int d_v, float* out, cudaStream_t stream);
+
+/* General form.  slot_begin == NULL selects the rank-major layout an
+ * all-gather produces: group g's splits are slots g + s*split_stride, s <
+ * n_splits.  state_out != 0 writes one partial slot per group instead of
+ * normalized rows (m = log2-sum-exp, l = 1, acc = normalized output; all-empty
+ * groups keep m = -inf, l = 0, acc = 0) -- a valid split state, so per-rank
+ * results can be all-gathered and merged again by this same call (the
+ * multi-GPU page-range split of SURVEY 8(e)). */
+int sphkv_lse_merge_ex(const float* partials, const int32_t* slot_begin, int n_splits,
+                       int64_t split_stride, int n_groups, int G, int d_v, float* out,
+                       int state_out, cudaStream_t stream);
 
 /* Bytes per partial slot for G query heads and d_v. */
 int64_t sphkv_partial_floats(int G, int d_v);

@@ -48,9 +48,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     cc = nvcc()
 
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")]
+    headers += [os.path.join(HERE, "..", "include", "sphkv_b200.h"), os.path.abspath(__file__)]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+
     def compile_one(item):
         src, extra = item
         obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        if (not force and os.path.exists(obj) and
+                os.path.getmtime(obj) >= max(newest_header,
+                                             os.path.getmtime(os.path.join(CSRC, src)))):
+            return obj  # incremental: object newer than its source and every header
         cmd = [cc, *ARCH, *COMMON, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:

@@ -17,7 +17,10 @@
 namespace sphkv {
 
 constexpr int LUT_MAX_BITS = 12;
-constexpr int LUT_BUDGET_BYTES = 90 * 1024;
+#ifndef SPHKV_LUT_KB
+#define SPHKV_LUT_KB 90
+#endif
+constexpr int LUT_BUDGET_BYTES = SPHKV_LUT_KB * 1024;
 
 // Polar (cos, sin) tables in shared memory, one per tier with B <= 12.
 //  * B <= 4: "pair" tables indexed by two consecutive items' codes (2B bits);

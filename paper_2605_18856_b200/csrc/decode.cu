@@ -32,7 +32,10 @@ constexpr float kLog2e = 1.4426950408889634f;
 #endif
 constexpr int ADA_NL = SPHKV_NL;   // logit warps
 constexpr int ADA_TI = 128;        // items per tile (4 per lane)
-constexpr int ADA_NS = 12;         // P slots
+#ifndef SPHKV_NS
+#define SPHKV_NS 12
+#endif
+constexpr int ADA_NS = SPHKV_NS;   // P slots
 constexpr int ADA_NV = 3;          // V slots
 #ifndef SPHKV_PF_MODE
 #define SPHKV_PF_MODE 0
@@ -49,6 +52,15 @@ constexpr int ADA_THREADS = (ADA_NL + ADA_NPV) * 32;
 constexpr int MAX_UNIT_TILES = 512;
 constexpr int PROW_PAD = 16;       // bytes of padding per P row (bank spread)
 
+struct FusedCtl {
+  const int32_t* slot_group;  // [n_slots] plan group of each partial slot, -1 = scratch
+  const int32_t* slot_begin;  // [n_groups + 1]
+  int32_t* ctl;
+  float* out;                 // [n_groups * G, d_v] normalized outputs
+  int n_groups;
+  int dynamic;                // units claimed from ctl[n_groups] instead of u += grid
+};
+
 struct AdaParams {
   sphkv_store_t st;
   const float* q;          // [groups, G, d] fp32
@@ -64,7 +76,8 @@ struct AdaParams {
   int TI;                   // tile items (min(P, 128))
   int dvp;                  // d_v padded to 16
   uint32_t smem_q, smem_tiles, smem_p, smem_v, smem_bar;  // byte offsets
-  int pslot_bytes, prow_bytes;
+  int pslot_bytes, prow_bytes, prows;  // P slot: prows rows of TI fp16 weights + header
+  FusedCtl fz;
 };
 
 __device__ __forceinline__ int tier_index(const sphkv_store_t& st, int tier_id) {
@@ -128,9 +141,10 @@ __device__ int build_tiles(const sphkv_store_t& st, const sphkv_unit_t& u, int T
 
 // Write the fp16 weights of one tile (4 items x G per lane) + tile max/sum.
 template <int NG>
-__device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int TI, int lane,
-                                            int G, const float lg[4][NG], int nvalid_lane) {
-  float* hdr = reinterpret_cast<float*>(slot + 8 * prow_bytes);
+__device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int prows, int TI,
+                                            int lane, int G, const float lg[4][NG],
+                                            int nvalid_lane) {
+  float* hdr = reinterpret_cast<float*>(slot + prows * prow_bytes);
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
     float m = -INFINITY;
@@ -181,8 +195,8 @@ __device__ __forceinline__ void pv_init(PVState<MTW>& s) {
 // ldmatrix.trans, B = fp16 weights of the P slot) + online combine.
 template <int MTW>
 __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, const uint8_t* vslot,
-                                        int prow_bytes, int TI, int dvp, int mt0, int mtn, int G,
-                                        int lane) {
+                                        int prow_bytes, int prows, int TI, int dvp, int mt0,
+                                        int mtn, int G, int lane) {
   float c[MTW][4];
 #pragma unroll
   for (int i = 0; i < MTW; ++i)
@@ -195,7 +209,10 @@ __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, c
   const int r = lane & 7, mat = lane >> 3;
   for (int ks = 0; ks < TI / 16; ++ks) {
     uint32_t b0, b1;
-    ptx::ldsm_x2(pbase + (lane & 7) * prow_bytes + (ks * 16 + ((lane >> 3) & 1) * 8) * 2, b0, b1);
+    // rows >= prows (only allocated when G > 4) alias the first rows: they feed
+    // mma columns g >= G, which are never read
+    ptx::ldsm_x2(pbase + ((lane & 7) & (prows - 1)) * prow_bytes +
+                     (ks * 16 + ((lane >> 3) & 1) * 8) * 2, b0, b1);
     const int item = ks * 16 + r + (mat >> 1) * 8;
 #pragma unroll
     for (int i = 0; i < MTW; ++i) {
@@ -208,7 +225,7 @@ __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, c
       }
     }
   }
-  const float* hdr = reinterpret_cast<const float*>(pslot + 8 * prow_bytes);
+  const float* hdr = reinterpret_cast<const float*>(pslot + prows * prow_bytes);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int g = 2 * (lane & 3) + h;
@@ -250,6 +267,89 @@ __device__ __forceinline__ void pv_write(const PVState<MTW>& s, float* part, int
 }
 
 // ---------------------------------------------------------------------------
+// In-kernel split merge + dynamic unit queue (shared by both decode kernels)
+// ---------------------------------------------------------------------------
+// With `slot_group` set, the CTA that completes the LAST split of a group
+// merges that group's partial slots straight into the output rows (the
+// split-K "last block" pattern): no separate merge launch, and the merge of
+// one group overlaps the other CTAs' decode.  ctl[] (caller-zeroed, left
+// zeroed): ctl[g] = finished splits of plan group g, ctl[n_groups] = unit
+// queue head, ctl[n_groups + 1] = CTAs done (the last one resets the queue).
+
+// Called by every thread after the unit's partial is written (all threads
+// have passed a __syncthreads since).  Returns through smem whether this CTA
+// merged; the caller's loop continues with *next_unit (dynamic mode).
+__device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* partials,
+                                                int out_slot, int G, int d_v, int n_units,
+                                                int* s_flag, float* s_ml, int* s_next) {
+  if (f.slot_group == nullptr && !f.dynamic) return;  // plain split partials only
+  __threadfence();  // this thread's partial writes -> gpu scope before the count
+  __syncthreads();
+  const int gi = (f.slot_group != nullptr) ? f.slot_group[out_slot] : -1;
+  if (threadIdx.x == 0) {
+    int last = 0;
+    if (gi >= 0) {
+      const int ns = f.slot_begin[gi + 1] - f.slot_begin[gi];
+      last = atomicAdd(&f.ctl[gi], 1) == ns - 1;
+    }
+    *s_flag = last;
+    if (f.dynamic) *s_next = atomicAdd(&f.ctl[f.n_groups], 1);
+  }
+  __syncthreads();
+  if (!*s_flag) return;
+  __threadfence();
+  const int b = f.slot_begin[gi], e = f.slot_begin[gi + 1];
+  const int64_t stride = (int64_t)G * (d_v + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int g = warp; g < G; g += nw) {  // (M, L) per query head
+    float M = -INFINITY;
+    for (int s = b + lane; s < e; s += 32) M = fmaxf(M, __ldcg(partials + s * stride + g));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f;
+    for (int s = b + lane; s < e; s += 32) {
+      const float m = __ldcg(partials + s * stride + g);
+      if (m != -INFINITY) L += __ldcg(partials + s * stride + G + g) * exp2f(m - M);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane == 0) {
+      s_ml[g] = M;
+      s_ml[8 + g] = L;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * d_v; i += blockDim.x) {
+    const int g = i / d_v, j = i % d_v;
+    const float M = s_ml[g], L = s_ml[8 + g];
+    float a = 0.f;
+    for (int s = b; s < e; ++s) {
+      const float m = __ldcg(partials + s * stride + g);
+      if (m != -INFINITY) a += __ldcg(partials + s * stride + 2 * G + (int64_t)g * d_v + j) * exp2f(m - M);
+    }
+    f.out[((int64_t)gi * G + g) * d_v + j] = (L > 0.f) ? a / L : 0.f;
+  }
+  if (threadIdx.x == 0) f.ctl[gi] = 0;  // every split of gi has counted: safe to re-arm
+  __syncthreads();
+}
+
+__device__ __forceinline__ int fused_first_unit(const FusedCtl& f, int* s_next) {
+  if (!f.dynamic) return blockIdx.x;
+  if (threadIdx.x == 0) *s_next = atomicAdd(&f.ctl[f.n_groups], 1);
+  __syncthreads();
+  return *s_next;
+}
+
+__device__ __forceinline__ void fused_kernel_exit(const FusedCtl& f) {
+  if (!f.dynamic || threadIdx.x != 0) return;
+  __threadfence();
+  if (atomicAdd(&f.ctl[f.n_groups + 1], 1) == (int)gridDim.x - 1) {
+    f.ctl[f.n_groups] = 0;  // every CTA has made its final claim
+    f.ctl[f.n_groups + 1] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // ADA kernel
 // ---------------------------------------------------------------------------
 template <int GP>
@@ -272,14 +372,11 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   const int d = st.d, P = st.page_size, TI = p.TI, dvp = p.dvp, MT = dvp / 16;
   const uint32_t vbytes = (uint32_t)TI * dvp * 2;
 
-  // polar LUTs (fp64 sincos rounded to fp32), barrier init
-  if (p.lut_global != nullptr) {
-    const uint4* src = reinterpret_cast<const uint4*>(p.lut_global);
-    uint4* dst = reinterpret_cast<uint4*>(smem);
-    for (int i = threadIdx.x; i < p.lut_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
-  } else {
-    lut_fill(smem, st.tiers, st.n_tiers, p.lut_off, threadIdx.x, blockDim.x);
-  }
+  // Prologue (independent of the previous grid, so under programmatic
+  // dependent launch it overlaps that grid's tail): barrier init and the
+  // polar LUTs -- one TMA bulk copy of the prebuilt tables (or fp64 sincos
+  // rounded to fp32 computed in place when the store has no global table).
+  uint64_t* lut_bar = bars + 2 * ADA_NS + 2 * ADA_NV;
   if (threadIdx.x == 0) {
     for (int i = 0; i < ADA_NS; ++i) {
       ptx::mbar_init(&p_full[i], 1);
@@ -289,12 +386,26 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       ptx::mbar_init(&v_full[i], 1);
       ptx::mbar_init(&v_empty[i], ADA_NPV);
     }
+    ptx::mbar_init(lut_bar, 1);
+    ptx::fence_mbar_init();
+    if (p.lut_global != nullptr && p.lut_bytes > 0) {
+      ptx::mbar_arrive_expect_tx(lut_bar, (uint32_t)p.lut_bytes);
+      ptx::bulk_g2s(smem, p.lut_global, (uint32_t)p.lut_bytes, lut_bar);
+    } else {
+      ptx::mbar_arrive(lut_bar);
+    }
   }
+  if (p.lut_global == nullptr) lut_fill(smem, st.tiers, st.n_tiers, p.lut_off, threadIdx.x, blockDim.x);
+  ptx::griddep_wait();  // inputs below (q, plan, store tables) may come from the previous grid
   __syncthreads();
+  ptx::griddep_launch_dependents();
+  bool lut_ready = false;
 
   const float qscale = kLog2e * rsqrtf((float)d);
+  __shared__ int s_flag, s_next;
+  __shared__ float s_ml[16];
   uint32_t gbase = 0;  // running tile sequence number (barrier phases)
-  for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+  for (int u = fused_first_unit(p.fz, &s_next); u < p.n_units;) {
     const sphkv_unit_t unit = p.units[u];
     if (warp == 0) {
       build_tiles(st, unit, TI, tiles, ntiles_s, lane);
@@ -313,6 +424,10 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 
     if (warp < ADA_NL) {
       // ---------------- logit warps ----------------
+      if (!lut_ready) {
+        ptx::mbar_wait(lut_bar, 0);
+        lut_ready = true;
+      }
       // tiles are claimed dynamically (smem counter) to balance the warps;
       // the P slot of tile k is k % NS whoever computes it.
       const uint64_t ppol = ptx::policy_evict_last();
@@ -363,7 +478,8 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         }
         const int ps = gk % ADA_NS;
         ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
-        write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, TI, lane, p.G, lg, nvalid);
+        write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, p.prows, TI, lane, p.G, lg,
+                            nvalid);
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
       }
@@ -398,7 +514,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         ptx::mbar_wait(&v_full[vs], (gk / ADA_NV) & 1);
         ptx::mbar_wait(&p_full[ps], (gk / ADA_NS) & 1);
         pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
-                         p.prow_bytes, TI, dvp, mt0, mtn, p.G, lane);
+                         p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane);
         __syncwarp();
         if (lane == 0) {
           ptx::mbar_arrive(&p_empty[ps]);
@@ -411,7 +527,11 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
     }
     gbase += nt;
     __syncthreads();
+    fused_unit_done(p.fz, p.partials, unit.out_slot, p.G, st.d_v, p.n_units, &s_flag, s_ml,
+                    &s_next);
+    u = p.fz.dynamic ? s_next : u + gridDim.x;
   }
+  fused_kernel_exit(p.fz);
 }
 
 // ---------------------------------------------------------------------------
@@ -434,6 +554,7 @@ struct DenseParams {
   int dp, dvp;            // padded key / value widths
   uint32_t smem_k, smem_v, smem_p, smem_bar;
   int pslot_bytes, prow_bytes;
+  FusedCtl fz;
 };
 
 __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParams p) {
@@ -458,11 +579,16 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
     for (int i = 0; i < DN_NK; ++i) { ptx::mbar_init(&k_full[i], 1); ptx::mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < DN_NV; ++i) { ptx::mbar_init(&v_full[i], 1); ptx::mbar_init(&v_empty[i], 1); }
     for (int i = 0; i < DN_NS; ++i) { ptx::mbar_init(&p_full[i], 1); ptx::mbar_init(&p_empty[i], 1); }
+    ptx::fence_mbar_init();
   }
+  ptx::griddep_wait();  // same PDL contract as the ADA kernel
   __syncthreads();
+  ptx::griddep_launch_dependents();
   const float qscale = kLog2e * rsqrtf((float)st.d);
+  __shared__ int s_flag, s_next;
+  __shared__ float s_ml[16];
   uint32_t gbase = 0;
-  for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {
+  for (int u = fused_first_unit(p.fz, &s_next); u < p.n_units;) {
     const sphkv_unit_t unit = p.units[u];
     const int t_begin = unit.ptr_begin * tiles_per_page;
     int t_end = unit.ptr_end * tiles_per_page;
@@ -563,7 +689,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
         const int vs = gk % DN_NV, ps = gk % DN_NS;
         ptx::mbar_wait(&v_full[vs], (gk / DN_NV) & 1);
         ptx::mbar_wait(&p_full[ps], (gk / DN_NS) & 1);
-        pv_tile<8>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes, p.prow_bytes,
+        pv_tile<8>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes, p.prow_bytes, 8,
                    DN_TI, dvp, 0, MT, p.G, lane);
         __syncwarp();
         if (lane == 0) {
@@ -589,33 +715,63 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
     }
     gbase += nt;
     __syncthreads();
+    fused_unit_done(p.fz, p.partials, unit.out_slot, p.G, st.d_v, p.n_units, &s_flag, s_ml,
+                    &s_next);
+    u = p.fz.dynamic ? s_next : u + gridDim.x;
   }
+  fused_kernel_exit(p.fz);
 }
 
 // ---------------------------------------------------------------------------
 // LSE merge
 // ---------------------------------------------------------------------------
+// Group grp's splits: slots [sb[grp], sb[grp+1]) when sb is given, else the
+// rank-major layout of an all-gather, slot = grp + s * split_stride for
+// s < n_splits.  state_out = 0: normalized output rows [n_groups*G][d_v];
+// state_out = 1: one partial slot per group (m = log2-sum-exp, l = 1,
+// acc = normalized output; an all-empty group stays m = -inf, l = 0, acc = 0),
+// which is again a valid split state for the next merge level.
 __global__ void k_lse_merge(const float* __restrict__ partials, const int32_t* __restrict__ sb,
-                            int n_groups, int G, int d_v, float* __restrict__ out) {
+                            int n_splits, int64_t split_stride, int n_groups, int G, int d_v,
+                            float* __restrict__ out, int state_out) {
   const int gid = blockIdx.x;  // group * G + g
   if (gid >= n_groups * G) return;
   const int grp = gid / G, g = gid % G;
-  const int b = sb[grp], e = sb[grp + 1];
+  int64_t b, step;
+  int cnt;
+  if (sb != nullptr) {
+    b = sb[grp];
+    cnt = sb[grp + 1] - sb[grp];
+    step = 1;
+  } else {
+    b = grp;
+    cnt = n_splits;
+    step = split_stride;
+  }
   const int64_t stride = (int64_t)G * (d_v + 2);
   float M = -INFINITY;
-  for (int s = b; s < e; ++s) M = fmaxf(M, partials[s * stride + g]);
+  for (int s = 0; s < cnt; ++s) M = fmaxf(M, partials[(b + s * step) * stride + g]);
   float L = 0.f;
-  for (int s = b; s < e; ++s) {
-    float m = partials[s * stride + g];
-    if (m != -INFINITY) L += partials[s * stride + G + g] * exp2f(m - M);
+  for (int s = 0; s < cnt; ++s) {
+    const float* ps = partials + (b + s * step) * stride;
+    float m = ps[g];
+    if (m != -INFINITY) L += ps[G + g] * exp2f(m - M);
   }
+  float* o = state_out ? out + (int64_t)grp * stride + 2 * G + (int64_t)g * d_v
+                       : out + (int64_t)gid * d_v;
   for (int j = threadIdx.x; j < d_v; j += blockDim.x) {
     float a = 0.f;
-    for (int s = b; s < e; ++s) {
-      float m = partials[s * stride + g];
-      if (m != -INFINITY) a += partials[s * stride + 2 * G + (int64_t)g * d_v + j] * exp2f(m - M);
+    for (int s = 0; s < cnt; ++s) {
+      const float* ps = partials + (b + s * step) * stride;
+      float m = ps[g];
+      if (m != -INFINITY) a += ps[2 * G + (int64_t)g * d_v + j] * exp2f(m - M);
     }
-    out[(int64_t)gid * d_v + j] = (L > 0.f) ? a / L : 0.f;
+    o[j] = (L > 0.f) ? a / L : 0.f;
+  }
+  if (state_out && threadIdx.x == 0) {
+    float* st = out + (int64_t)grp * stride;
+    st[g] = (L > 0.f) ? M + log2f(L) : -INFINITY;
+    st[G + g] = (L > 0.f) ? 1.f : 0.f;
   }
 }
 
@@ -655,19 +811,39 @@ extern "C" int sphkv_store_build_lut(sphkv_store_t* st, cudaStream_t stream) {
   return SPHKV_OK;
 }
 
-template <int GP>
-static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
-  auto kern = k_ada_decode<GP>;
-  SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<grid, ADA_THREADS, smem, stream>>>(p);
+// Launch with programmatic stream serialization (PDL): the kernel's
+// prologue may start while the previous grid on the stream drains; it waits
+// (griddepcontrol.wait) before touching any input.
+template <typename Kern, typename Params>
+static int launch_pdl(Kern kern, const Params& p, int grid, int threads, size_t smem,
+                      cudaStream_t stream) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  SPHKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
   SPHKV_LAUNCH_CHECK();
   return SPHKV_OK;
 }
 
-extern "C" int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
-                                const sphkv_unit_t* units, int n_units, float* partials,
-                                float* logits_dbg, const int64_t* dbg_offsets, int grid,
-                                cudaStream_t stream) {
+template <int GP>
+static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
+  auto kern = k_ada_decode<GP>;
+  SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream);
+}
+
+static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
+                           const sphkv_unit_t* units, int n_units, float* partials,
+                           float* logits_dbg, const int64_t* dbg_offsets, int grid,
+                           const FusedCtl& fz, cudaStream_t stream) {
   if (!st || !q || !units || !partials) return fail(SPHKV_E_VALUE, "null argument");
   if (G < 1 || G > 8) return fail(SPHKV_E_UNSUPPORTED, "GQA group size %d outside [1, 8]", G);
   if (st->d < 3 || st->d > 256) return fail(SPHKV_E_UNSUPPORTED, "d=%d outside [3, 256]", st->d);
@@ -691,6 +867,7 @@ extern "C" int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
   p.partials = partials;
   p.logits_dbg = logits_dbg;
   p.dbg_off = dbg_offsets;
+  p.fz = fz;
   p.TI = st->page_size < ADA_TI ? st->page_size : ADA_TI;
   p.dvp = (st->d_v + 15) / 16 * 16;
   int used = lut_layout(st, p.lut_off);
@@ -708,29 +885,35 @@ extern "C" int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
   p.smem_tiles = (uint32_t)off;
   off = align_up(off + MAX_UNIT_TILES * sizeof(TileEntry) + 16, 128);
   p.prow_bytes = p.TI * 2 + PROW_PAD;
-  p.pslot_bytes = (int)align_up(8 * p.prow_bytes + 64, 128);
+  p.prows = G <= 4 ? 4 : 8;
+  p.pslot_bytes = (int)align_up(p.prows * p.prow_bytes + 64, 128);
   p.smem_p = (uint32_t)off;
   off += (size_t)ADA_NS * p.pslot_bytes;
   off = align_up(off, 1024);
   p.smem_v = (uint32_t)off;
   off += (size_t)ADA_NV * p.TI * p.dvp * 2;
   p.smem_bar = (uint32_t)off;
-  off += (2 * ADA_NS + 2 * ADA_NV) * 8;
+  off += (2 * ADA_NS + 2 * ADA_NV + 1) * 8;
   size_t smem = off;
   if (smem > 227 * 1024) return fail(SPHKV_E_UNSUPPORTED, "ADA smem %zu exceeds 227 KB", smem);
   if (grid <= 0) grid = SM_COUNT;
   if (grid > n_units) grid = n_units;
+#ifdef SPHKV_ONLY_GP  // fast experimental builds: one GQA width only
+  if (GP != SPHKV_ONLY_GP) return fail(SPHKV_E_UNSUPPORTED, "built for GP=%d only", SPHKV_ONLY_GP);
+  return launch_ada<SPHKV_ONLY_GP>(p, smem, grid, stream);
+#else
   switch (GP) {
     case 1: return launch_ada<1>(p, smem, grid, stream);
     case 2: return launch_ada<2>(p, smem, grid, stream);
     case 3: return launch_ada<3>(p, smem, grid, stream);
     default: return launch_ada<4>(p, smem, grid, stream);
   }
+#endif
 }
 
-extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,
-                                  const sphkv_unit_t* units, int n_units, float* partials,
-                                  int grid, cudaStream_t stream) {
+static int dense_decode_impl(const sphkv_dense_store_t* st, const float* q, int G,
+                             const sphkv_unit_t* units, int n_units, float* partials, int grid,
+                             const FusedCtl& fz, cudaStream_t stream) {
   if (!st || !q || !units || !partials) return fail(SPHKV_E_VALUE, "null argument");
   if (G < 1 || G > 8) return fail(SPHKV_E_UNSUPPORTED, "GQA group size %d outside [1, 8]", G);
   if (st->d > 128 || st->d_v > 128) return fail(SPHKV_E_UNSUPPORTED, "d/d_v above 128");
@@ -744,6 +927,7 @@ extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q,
   p.units = units;
   p.n_units = n_units;
   p.partials = partials;
+  p.fz = fz;
   p.dp = (st->d + 15) / 16 * 16;
   p.dvp = (st->d_v + 15) / 16 * 16;
   p.prow_bytes = DN_TI * 2 + PROW_PAD;
@@ -766,17 +950,82 @@ extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q,
                                       (int)smem));
   if (grid <= 0) grid = SM_COUNT;
   if (grid > n_units) grid = n_units;
-  k_dense_decode<<<grid, DN_THREADS, smem, stream>>>(p);
+  return launch_pdl(k_dense_decode, p, grid, DN_THREADS, smem, stream);
+}
+
+static int make_fused(FusedCtl& f, const int32_t* slot_group, const int32_t* slot_begin,
+                      int n_groups, int32_t* ctl, float* out, int dynamic) {
+  memset(&f, 0, sizeof(f));
+  if (slot_group != nullptr && (!slot_begin || !ctl || !out || n_groups < 1))
+    return fail(SPHKV_E_VALUE, "fused merge needs slot_begin, ctl and out");
+  if (dynamic && !ctl) return fail(SPHKV_E_VALUE, "dynamic unit queue needs ctl");
+  f.slot_group = slot_group;
+  f.slot_begin = slot_begin;
+  f.ctl = ctl;
+  f.out = out;
+  f.n_groups = n_groups;
+  f.dynamic = dynamic;
+  return SPHKV_OK;
+}
+
+extern "C" int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
+                                const sphkv_unit_t* units, int n_units, float* partials,
+                                float* logits_dbg, const int64_t* dbg_offsets, int grid,
+                                cudaStream_t stream) {
+  FusedCtl f;
+  make_fused(f, nullptr, nullptr, 0, nullptr, nullptr, 0);
+  return ada_decode_impl(st, q, G, units, n_units, partials, logits_dbg, dbg_offsets, grid, f,
+                         stream);
+}
+
+extern "C" int sphkv_ada_decode_fused(const sphkv_store_t* st, const float* q, int G,
+                                      const sphkv_unit_t* units, int n_units, float* partials,
+                                      const int32_t* slot_group, const int32_t* slot_begin,
+                                      int n_groups, int32_t* ctl, float* out, int dynamic,
+                                      int grid, cudaStream_t stream) {
+  FusedCtl f;
+  int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
+  if (rc) return rc;
+  return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream);
+}
+
+extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,
+                                  const sphkv_unit_t* units, int n_units, float* partials,
+                                  int grid, cudaStream_t stream) {
+  FusedCtl f;
+  make_fused(f, nullptr, nullptr, 0, nullptr, nullptr, 0);
+  return dense_decode_impl(st, q, G, units, n_units, partials, grid, f, stream);
+}
+
+extern "C" int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const float* q, int G,
+                                        const sphkv_unit_t* units, int n_units, float* partials,
+                                        const int32_t* slot_group, const int32_t* slot_begin,
+                                        int n_groups, int32_t* ctl, float* out, int dynamic,
+                                        int grid, cudaStream_t stream) {
+  FusedCtl f;
+  int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
+  if (rc) return rc;
+  return dense_decode_impl(st, q, G, units, n_units, partials, grid, f, stream);
+}
+
+extern "C" int sphkv_lse_merge_ex(const float* partials, const int32_t* slot_begin,
+                                  int n_splits, int64_t split_stride, int n_groups, int G,
+                                  int d_v, float* out, int state_out, cudaStream_t stream) {
+  if (!partials || !out) return fail(SPHKV_E_VALUE, "null argument");
+  if (!slot_begin && (n_splits < 0 || split_stride < n_groups))
+    return fail(SPHKV_E_VALUE, "bad split layout (n_splits=%d, stride=%lld)", n_splits,
+                (long long)split_stride);
+  if (G < 1 || d_v < 1) return fail(SPHKV_E_VALUE, "bad G/d_v");
+  if (n_groups == 0) return SPHKV_OK;
+  int threads = d_v >= 128 ? 128 : ((d_v + 31) / 32) * 32;
+  k_lse_merge<<<n_groups * G, threads, 0, stream>>>(partials, slot_begin, n_splits, split_stride,
+                                                    n_groups, G, d_v, out, state_out);
   SPHKV_LAUNCH_CHECK();
   return SPHKV_OK;
 }
 
 extern "C" int sphkv_lse_merge(const float* partials, const int32_t* slot_begin, int n_groups,
                                int G, int d_v, float* out, cudaStream_t stream) {
-  if (!partials || !slot_begin || !out) return fail(SPHKV_E_VALUE, "null argument");
-  if (n_groups == 0) return SPHKV_OK;
-  int threads = d_v >= 128 ? 128 : ((d_v + 31) / 32) * 32;
-  k_lse_merge<<<n_groups * G, threads, 0, stream>>>(partials, slot_begin, n_groups, G, d_v, out);
-  SPHKV_LAUNCH_CHECK();
-  return SPHKV_OK;
+  if (!slot_begin) return fail(SPHKV_E_VALUE, "null argument");
+  return sphkv_lse_merge_ex(partials, slot_begin, 0, 0, n_groups, G, d_v, out, 0, stream);
 }

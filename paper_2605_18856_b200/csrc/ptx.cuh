@@ -88,6 +88,18 @@ __device__ __forceinline__ void prefetch_l2_line(const void* p) {
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+// mbarrier inits visible to the async (TMA) proxy before the first bulk copy
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// Programmatic dependent launch: wait for the preceding grid (no-op when the
+// kernel was launched without the PDL attribute) / let the next grid launch.
+__device__ __forceinline__ void griddep_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 // ---- ldmatrix / mma -------------------------------------------------------
 __device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1,

@@ -62,10 +62,15 @@ def ada_decode(store, q, plan: DecodePlan | None = None, *, out=None, partials=N
         out = torch.empty((ng * G, store.d_v), dtype=torch.float32, device="cuda")
     sp = _lib.stream_ptr(stream)
     # q rows are addressed by absolute group id inside the kernel
+    if logits is None:  # one launch: the last split of each group merges it in-kernel
+        _lib.check(l.sphkv_ada_decode_fused(
+            store.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
+            partials.data_ptr(), plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng,
+            plan.ctl.data_ptr(), out.data_ptr(), int(plan.dynamic), plan.grid, sp))
+        return out
     _lib.check(l.sphkv_ada_decode(store.cptr, q.data_ptr(), G, plan.units.data_ptr(),
                                   plan.n_units, partials.data_ptr(), _lib.ptr(logits),
-                                  plan.dbg_offsets.data_ptr() if logits is not None else None,
-                                  plan.grid, sp))
+                                  plan.dbg_offsets.data_ptr(), plan.grid, sp))
     _lib.check(l.sphkv_lse_merge(partials.data_ptr(), plan.slot_begin.data_ptr(), ng, G,
                                  store.d_v, out.data_ptr(), sp))
     return out
@@ -85,10 +90,10 @@ def dense_decode(dstore, q, plan: DecodePlan | None = None, *, out=None, partial
     if out is None:
         out = torch.empty((ng * G, dstore.d_v), dtype=torch.float32, device="cuda")
     sp = _lib.stream_ptr(stream)
-    _lib.check(l.sphkv_dense_decode(dstore.cptr, q.data_ptr(), G, plan.units.data_ptr(),
-                                    plan.n_units, partials.data_ptr(), plan.grid, sp))
-    _lib.check(l.sphkv_lse_merge(partials.data_ptr(), plan.slot_begin.data_ptr(), ng, G,
-                                 dstore.d_v, out.data_ptr(), sp))
+    _lib.check(l.sphkv_dense_decode_fused(
+        dstore.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units, partials.data_ptr(),
+        plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng, plan.ctl.data_ptr(),
+        out.data_ptr(), int(plan.dynamic), plan.grid, sp))
     return out
 
 

@@ -25,7 +25,8 @@ PAGE_HEADER_BYTES = 16
 
 
 class DecodePlan:
-    def __init__(self, units, slot_begin, n_slots, grid, group_items, group_ids, dbg_offsets):
+    def __init__(self, units, slot_begin, n_slots, grid, group_items, group_ids, dbg_offsets,
+                 slot_group=None, dynamic=False):
         import torch
 
         self.units_host = units
@@ -39,6 +40,14 @@ class DecodePlan:
         self.group_ids = group_ids          # planned groups, merge order
         self.dbg_offsets_host = dbg_offsets
         self.dbg_offsets = torch.as_tensor(dbg_offsets, device="cuda")
+        self.dynamic = dynamic
+        # fused in-kernel merge: plan group of every partial slot (+ scratch = -1)
+        # and the caller-zeroed control words (sphkv_ada_decode_fused)
+        sg = np.full(n_slots + 1, -1, dtype=np.int32)
+        if slot_group is not None:
+            sg[:n_slots] = slot_group
+        self.slot_group = torch.as_tensor(sg, device="cuda")
+        self.ctl = torch.zeros(len(group_ids) + 2, dtype=torch.int32, device="cuda")
 
 
 def _page_bytes(rows, tiers, d, d_v, P):
@@ -51,34 +60,133 @@ def _page_bytes(rows, tiers, d, d_v, P):
     return PAGE_HEADER_BYTES + code + 2 * c * d_v, -(-c // ti)
 
 
-def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2) -> DecodePlan:
-    """Plan a decode pass over `groups` (default: every group of the store)."""
+# Planner cost of one retained item beyond its stream bytes: the logit work of
+# an ADA item (127 LUT/FMA rows) takes about as long as streaming this many
+# bytes at the kernel's rate, so units are balanced on bytes + ITEM_COST*items.
+ITEM_COST = 160
+
+
+def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
+               dynamic=False) -> DecodePlan:
+    """Plan a decode pass over `groups` (default: every group of the store).
+
+    `ranges` (optional, one (begin, end) per group) restricts each group to a
+    contiguous range of its pointer list -- the page-range split of one
+    sequence across ranks; see `plan_store_range`."""
     n, rows, plen, ptr = store._host()
     if groups is None:
         groups = np.arange(store.groups)
     groups = np.asarray(groups, dtype=np.int64)
+    if ranges is None:
+        ranges = [(0, int(plen[g])) for g in groups]
     pbytes, ptiles = _page_bytes(rows, store.tiers, store.d, store.d_v, store.page_size)
-    lists = [ptr[g, : plen[g]] for g in groups]
+    pbytes = pbytes + ITEM_COST * rows["count"].astype(np.int64)
+    lists = [ptr[g, rb:re] for g, (rb, re) in zip(groups, ranges)]
     total = sum(int(pbytes[l].sum()) for l in lists)
     target = max(total // max(grid * units_per_cta, 1), 1)
     pieces = []  # (bytes, group, begin, end, piece index)
-    for gi, (g, lst) in enumerate(zip(groups, lists)):
+    if units_per_cta == 1 and 0 < len(groups) <= grid and total > 0:
+        # one unit per CTA: give each group a share of the grid proportional
+        # to its cost (largest remainder) and cut its list at the cost
+        # quantiles, so every CTA gets ~total/grid and none gets two pieces
+        gcost = np.array([int(pbytes[l].sum()) for l in lists], dtype=np.float64)
+        share = gcost / gcost.sum() * grid
+        n_g = np.floor(share).astype(np.int64)
+        n_g = np.where((gcost > 0) & (n_g == 0), 1, n_g)
+        rem = grid - int(n_g.sum())
+        for i in np.argsort(-(share - np.floor(share)), kind="stable")[:max(rem, 0)]:
+            n_g[i] += 1
+        for g, lst, (rb, _), n in zip(groups, lists, ranges, n_g):
+            if len(lst) == 0:
+                pieces.append([0, int(g), rb, rb])
+                continue
+            c = np.cumsum(pbytes[lst])
+            cuts = [0] + [int(np.searchsorted(c, c[-1] * k / n, side="left")) + 1
+                          for k in range(1, int(n))] + [len(lst)]
+            cuts = np.minimum(np.maximum.accumulate(cuts), len(lst))
+            for s0, e0 in zip(cuts[:-1], cuts[1:]):
+                if e0 > s0:
+                    while int(ptiles[lst[s0:e0]].sum()) > MAX_UNIT_TILES:  # tile cap
+                        m = s0 + max(1, (e0 - s0) // 2)
+                        pieces.append([int(pbytes[lst[s0:m]].sum()), int(g), rb + s0, rb + m])
+                        s0 = m
+                    pieces.append([int(pbytes[lst[s0:e0]].sum()), int(g), rb + s0, rb + e0])
+        lists = []  # done
+    for g, lst, (rb, _) in zip(groups, lists, ranges):
         b = pbytes[lst] if len(lst) else np.zeros(0, np.int64)
         t = ptiles[lst] if len(lst) else np.zeros(0, np.int64)
         start, acc, tacc = 0, 0, 0
         for k in range(len(lst)):
             if k > start and (acc + b[k] > target * 1.05 or tacc + t[k] > MAX_UNIT_TILES):
-                pieces.append([acc, int(g), start, k])
+                pieces.append([acc, int(g), rb + start, rb + k])
                 start, acc, tacc = k, 0, 0
             acc += int(b[k])
             tacc += int(t[k])
-        pieces.append([acc, int(g), start, len(lst)])  # (possibly empty group)
-    return _finish(pieces, groups, grid, lambda g: int(rows["count"][ptr[g, : plen[g]]].sum())
-                   if plen[g] else 0, lambda g, s, e: int(rows["count"][ptr[g, s:e]].sum())
-                   if e > s else 0)
+        pieces.append([acc, int(g), rb + start, rb + len(lst)])  # (possibly empty group)
+    rng = {int(g): r for g, r in zip(groups, ranges)}
+    return _finish(pieces, groups, grid,
+                   lambda g: int(rows["count"][ptr[g, rng[g][0]:rng[g][1]]].sum()),
+                   lambda g, s: int(rows["count"][ptr[g, rng[g][0]:s]].sum()) if s > rng[g][0]
+                   else 0, dynamic)
 
 
-def plan_dense(dstore, groups=None, grid=SM_COUNT, units_per_cta=2) -> DecodePlan:
+def split_ranges(page_bytes, world):
+    """Split one pointer list (per-page stream bytes, pointer order) into
+    `world` contiguous ranges balanced by bytes, not page count (tiers differ
+    in bytes per item).  Range r ends at the first page whose cumulative bytes
+    reach (r+1)/world of the total; ranges may be empty."""
+    b = np.asarray(page_bytes, dtype=np.int64)
+    n = len(b)
+    if n == 0:
+        return [(0, 0)] * world
+    c = np.cumsum(b)
+    tot = int(c[-1])
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(np.searchsorted(c, tot * r / world, side="left")) + 1
+                    if tot > 0 else (n * r) // world)
+    cuts.append(n)
+    cuts = np.minimum(np.maximum.accumulate(cuts), n)
+    return [(int(cuts[r]), int(cuts[r + 1])) for r in range(world)]
+
+
+def rank_ranges(store, groups, rank, world):
+    """This rank's pointer-list range of every group (page-range split)."""
+    n, rows, plen, ptr = store._host()
+    pbytes, _ = _page_bytes(rows, store.tiers, store.d, store.d_v, store.page_size)
+    return [split_ranges(pbytes[ptr[g, : plen[g]]], world)[rank] for g in groups]
+
+
+def plan_store_range(store, groups, rank, world, grid=SM_COUNT, units_per_cta=2,
+                     dynamic=False) -> DecodePlan:
+    """Rank `rank`'s share of a page-range split of `groups` over `world` ranks.
+
+    The rank's units cover only its ranges; `sphkv_lse_merge_ex(state_out=1)`
+    turns its splits into one partial state per (group, q-head), those are
+    all-gathered (rank-major) and merged again -- `merge_gathered`."""
+    groups = np.asarray(groups, dtype=np.int64)
+    return plan_store(store, groups, grid, units_per_cta,
+                      ranges=rank_ranges(store, groups, rank, world), dynamic=dynamic)
+
+
+def merge_local_state(plan, partials, G, d_v, state_out, stream=None):
+    """Merge this rank's splits into one partial slot per planned group."""
+    l = _lib.lib()
+    _lib.check(l.sphkv_lse_merge_ex(partials.data_ptr(), plan.slot_begin.data_ptr(), 0, 0,
+                                    len(plan.group_ids), G, d_v, state_out.data_ptr(), 1,
+                                    _lib.stream_ptr(stream)))
+    return state_out
+
+
+def merge_gathered(n_groups, world, gathered, G, d_v, out, stream=None):
+    """Merge the rank-major all-gather [world][n_groups] of per-rank states."""
+    l = _lib.lib()
+    _lib.check(l.sphkv_lse_merge_ex(gathered.data_ptr(), None, world, n_groups, n_groups, G,
+                                    d_v, out.data_ptr(), 0, _lib.stream_ptr(stream)))
+    return out
+
+
+def plan_dense(dstore, groups=None, grid=SM_COUNT, units_per_cta=2, dynamic=False) -> DecodePlan:
     """Same planner for the dense baseline store (uniform pages)."""
     G = dstore.batch * dstore.layers * dstore.heads
     if groups is None:
@@ -98,10 +206,10 @@ def plan_dense(dstore, groups=None, grid=SM_COUNT, units_per_cta=2) -> DecodePla
             pieces.append([max(items, 0) * (dstore.d + dstore.d_v) * 2, int(g), s, e])
     T = dstore.tokens
     return _finish(pieces, groups, grid, lambda g: T,
-                   lambda g, s, e: max(min(e * P, T) - s * P, 0))
+                   lambda g, s: max(min(s * P, T), 0), dynamic)
 
 
-def _finish(pieces, groups, grid, group_items_fn, piece_items_fn):
+def _finish(pieces, groups, grid, group_items_fn, piece_items_fn, dynamic=False):
     # consecutive partial slots per group in `groups` order
     order = {int(g): i for i, g in enumerate(groups)}
     pieces.sort(key=lambda p: (order[p[1]], p[2]))
@@ -114,6 +222,18 @@ def _finish(pieces, groups, grid, group_items_fn, piece_items_fn):
     # debug logit offsets (items before this piece in planned-group order)
     gi_items = np.array([group_items_fn(int(g)) for g in groups], dtype=np.int64)
     g_off = np.concatenate([[0], np.cumsum(gi_items)])
+    slot_group = np.array([order[p[1]] for p in pieces], dtype=np.int32)
+    if dynamic:
+        # CTAs claim units from a global queue in list order: longest first
+        units, dbg = [], []
+        for _, g, s, e, slot in sorted(pieces, key=lambda p: (-p[0], p[4])):
+            units.append((g, s, e, slot))
+            dbg.append(g_off[order[g]] + piece_items_fn(g, s))
+        arr = np.array(units, dtype=np.int32).reshape(-1, 4)
+        u = np.zeros(len(arr), dtype=_lib.UNIT_DTYPE)
+        u["group"], u["ptr_begin"], u["ptr_end"], u["out_slot"] = arr.T
+        return DecodePlan(u, slot_begin, n_slots, max(1, min(grid, len(pieces))), gi_items,
+                          groups, np.asarray(dbg, dtype=np.int64), slot_group, True)
     # LPT bin packing onto the CTAs
     grid = max(1, min(grid, len(pieces)))
     heap = [(0, c) for c in range(grid)]
@@ -130,7 +250,7 @@ def _finish(pieces, groups, grid, group_items_fn, piece_items_fn):
             if r < len(bins[c]):
                 _, g, s, e, slot = bins[c][r]
                 units.append((g, s, e, slot))
-                dbg.append(g_off[order[g]] + piece_items_fn(g, 0, s))
+                dbg.append(g_off[order[g]] + piece_items_fn(g, s))
             else:
                 units.append((int(groups[0]) if len(groups) else 0, 0, 0, scratch))
                 dbg.append(0)
@@ -138,4 +258,4 @@ def _finish(pieces, groups, grid, group_items_fn, piece_items_fn):
     u = np.zeros(len(arr), dtype=_lib.UNIT_DTYPE)
     u["group"], u["ptr_begin"], u["ptr_end"], u["out_slot"] = arr.T
     return DecodePlan(u, slot_begin, n_slots, grid, gi_items, groups,
-                      np.asarray(dbg, dtype=np.int64))
+                      np.asarray(dbg, dtype=np.int64), slot_group, False)

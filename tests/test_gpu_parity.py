@@ -234,6 +234,45 @@ def test_split_merge_equals_single_pass(sk):
     assert torch.allclose(one, many, rtol=2e-5, atol=2e-5)
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_page_range_split_two_level_merge(sk, world):
+    """Multi-GPU data path on one device: each simulated rank decodes its
+    page range (plan_store_range), merges its splits to one state per
+    (group, q-head) (lse_merge_ex state_out=1), the states are laid out rank-
+    major as all_gather_into_tensor produces them, and merge_gathered must
+    equal the single-pass decode."""
+    import torch
+    from paper_2605_18856_b200 import _lib, plan as planmod
+
+    wl = sk.synth.generate(1, 2, 2, 4, 3000, 64, seed=5)
+    tiers = table(sk, [(0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8), (3, 12, 14, 8)])
+    st = sk.PagedStore(tiers, 2, 2, 64, 64, 128, capacity_tokens=3000)
+    n = wl.groups * wl.tokens
+    rng = np.random.default_rng(2)
+    tier = rng.choice([0, 1, 2, 3], n, p=[0.1, 0.4, 0.4, 0.1]).astype(np.int16)
+    radii = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().sphkv_encode_radii(wl.keys.data_ptr(), _lib.BF16, n, 64,
+                                             radii.data_ptr(), _lib.stream_ptr()))
+    sk.pack_device(st, keys=wl.keys.view(-1, 64), radii=radii, values=wl.values.view(-1, 64),
+                   z=(tier != 0).astype(np.int8), tier=tier, protect=np.zeros(n, np.uint8),
+                   tokens=wl.tokens)
+    groups = list(range(wl.groups))
+    want = sk.ada_decode(st, wl.queries, sk.plan_store(st, groups=groups))
+    G, dv = 4, 64
+    F = G * (dv + 2)
+    gathered = torch.empty((world, len(groups), F), dtype=torch.float32, device="cuda")
+    for r in range(world):
+        p = planmod.plan_store_range(st, groups, r, world, grid=16)
+        parts = sk.decode._partials(p, G, dv)
+        _lib.check(_lib.lib().sphkv_ada_decode(st.cptr, wl.queries.data_ptr(), G,
+                                               p.units.data_ptr(), p.n_units, parts.data_ptr(),
+                                               None, None, p.grid, _lib.stream_ptr()))
+        planmod.merge_local_state(p, parts, G, dv, gathered[r])
+    out = torch.empty_like(want)
+    planmod.merge_gathered(len(groups), world, gathered, G, dv, out)
+    assert torch.allclose(out, want, rtol=2e-5, atol=2e-5)
+
+
 def test_config1_geometry_vs_oracle(sk):
     """1 layer, 8 KV / 32 Q heads, d=128, T=8K, P=256, panel tiers, RDR at a
     ~30% KV-byte reduction: page bytes exact, attend within tolerance."""
