@@ -14,13 +14,18 @@
  * would add on the reference side.
  *
  * Device page format:
- *   code pool  : per page a 16-byte aligned block = (d-1) angle rows of
- *                page_size*angle_bits bits (coordinate-major, LSB-first, the
- *                reference SoA stream of store.py:205-208 with stride
- *                page_size) followed by one radius row of page_size*radius_bits
- *                bits, padded to 16 bytes.  For a full page the angle rows are
- *                byte-identical to Page.angle_stream(); partial pages are
- *                re-strided by sphkv_export_streams().
+ *   code pool  : per page a 16-byte aligned block.  Angle part, "word-
+ *                interleaved item-major": item i's d-1 codes are one LSB-first
+ *                bit string (code j at bits [j*b, j*b+b)) padded to W words
+ *                (ceil((d-1)*b/32) rounded up to a multiple of 4); 16-byte
+ *                quad w4 of item i is stored at quad ((i/32)*(W/4) + w4)*32 +
+ *                i%32 (granules of 32 items: a warp loads one quad of 32 items
+ *                as one coalesced 512-byte load and each lane holds its item's
+ *                codes in registers).
+ *                Then one radius row of page_size*radius_bits bits (LSB-
+ *                first), padded to 16 bytes.  sphkv_export_streams() converts
+ *                to the reference's coordinate-major SoA streams
+ *                (store.py:205-211) bit for bit.
  *   value pool : fp16 [page][page_size][d_v]; inside each row the 16-byte
  *                chunk c of item i is stored at chunk (c ^ (i & 7)) so that
  *                1-D bulk copies land ldmatrix-conflict-free in shared memory.

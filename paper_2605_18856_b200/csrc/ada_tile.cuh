@@ -1,5 +1,6 @@
-// ADA logit tile: logits of 4 consecutive page items per lane, straight from
-// the angle/radius codes (decode.py:123-192: l = (r_q/sqrt d) r~ (feat.qfeat)).
+// ADA logit tile: logits of a 128-item tile (lane l owns items l, l+32, l+64,
+// l+96), straight from the angle/radius codes (decode.py:123-192:
+// l = (r_q/sqrt d) r~ (feat . qfeat)).
 //
 // The feature row of an item is the recurrence f_j = (prod_{l<j} sin a_l) cos a_j
 // (codec.py:459-477); the kernel never forms it in memory: per code row it
@@ -10,9 +11,7 @@
 #include "common.cuh"
 #include "ptx.cuh"
 
-#ifndef SPHKV_RING
-#define SPHKV_RING 1
-#endif
+#include <utility>
 
 namespace sphkv {
 
@@ -23,8 +22,11 @@ constexpr int LUT_MAX_BITS = 12;
 constexpr int LUT_BUDGET_BYTES = SPHKV_LUT_KB * 1024;
 
 // Polar (cos, sin) tables in shared memory, one per tier with B <= 12.
-//  * B <= 4: "pair" tables indexed by two consecutive items' codes (2B bits);
-//    an entry (cos a, cos b, sin a, sin b) is one LDS.128 feeding packed FMUL2.
+//  * B <= 4: "row-pair" tables indexed by the codes of two consecutive rows
+//    (j, j+1) of the same item (2B contiguous bits of its code string); an
+//    entry (cos a_j, sin a_j cos a_j+1, sin a_j sin a_j+1, 0) -- products
+//    taken in fp64, rounded once -- is one LDS.128 that advances the feature
+//    recurrence by two rows.
 //  * 5 <= B <= 12: single-code tables, entry (cos, sin) = one LDS.64.
 // Random gathers from a small table bank-conflict heavily, so when the budget
 // allows a table is stored REP times interleaved: entry e of copy r lives at
@@ -71,8 +73,7 @@ __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n
   return used;
 }
 
-// Fill byte range [i*16, i*16+16) ... one entry copy per call: tier bits B,
-// entry e, copy r of a table starting at `dst`.
+// Fill one (entry, copy) of a table: tier bits B, entry e, copy r.
 __device__ inline void lut_write_entry(uint8_t* dst, int B, bool repl, int e, int r) {
   const double step = kPi / (double)((1u << B) - 1u);
   const int R = repl ? lut_rep(B) : 1;
@@ -85,12 +86,12 @@ __device__ inline void lut_write_entry(uint8_t* dst, int B, bool repl, int e, in
   } else {
     const uint32_t M = (1u << B) - 1u;
     double sa, ca, sb, cb;
-    sincos((double)(e & M) * step, &sa, &ca);
-    sincos((double)((e >> B) & M) * step, &sb, &cb);
+    sincos((double)(e & M) * step, &sa, &ca);          // row j   (low B bits)
+    sincos((double)((e >> B) & M) * step, &sb, &cb);   // row j+1 (high B bits)
     out[0] = (float)ca;
-    out[1] = (float)cb;
-    out[2] = (float)sa;
-    out[3] = (float)sb;
+    out[1] = (float)(sa * cb);
+    out[2] = (float)(sa * sb);
+    out[3] = 0.f;
   }
 }
 
@@ -108,51 +109,14 @@ __device__ inline void lut_fill(uint8_t* lut, const sphkv_tier_t* tiers, int n_t
   }
 }
 
-template <int B>
-struct CodeWin {
-  // max over lanes of the in-word shift of a lane's 4 codes (4 * lane * B mod 32)
-  static constexpr int MAXSH = (B % 2) ? 28 : ((B % 4) ? 24 : ((B % 8) ? 16 : 0));
-  static constexpr int WORDS = (4 * B <= 32 && MAXSH + 4 * B <= 32) ? 1
-                             : (MAXSH + 4 * B <= 64 ? 2 : 3);
-};
-
-// 64-bit window of a lane's 4 codes starting at bit `sh` of its first word
-template <int B>
-__device__ __forceinline__ uint64_t code_window(const uint32_t (&r)[CodeWin<B>::WORDS], int sh) {
-  if constexpr (CodeWin<B>::WORDS == 1) {
-    return (uint64_t)(r[0] >> sh);
-  } else if constexpr (CodeWin<B>::WORDS == 2) {
-    const uint32_t a = __funnelshift_r(r[0], r[1], sh);
-    return ((uint64_t)(r[1] >> sh) << 32) | a;
-  } else {
-    const uint32_t a = __funnelshift_r(r[0], r[1], sh);
-    const uint32_t b = __funnelshift_r(r[1], r[2], sh);
-    return ((uint64_t)b << 32) | a;
-  }
-}
-
-template <int B>
-__device__ __forceinline__ uint32_t code_at(uint64_t y, int k) {
-  return (uint32_t)(y >> (k * B)) & ((1u << B) - 1u);
-}
-
-// Shared-memory reads are plain C++ loads through pointers into the kernel's
-// extern __shared__ buffer (the compiler emits LDS and, unlike non-volatile
-// asm, keeps them ordered after the barriers that publish the data).
-__device__ __forceinline__ float2 lds_f2(const uint8_t* sm, uint32_t off) {
-  return *reinterpret_cast<const float2*>(sm + off);
-}
-__device__ __forceinline__ void lds_pair2(const uint8_t* sm, uint32_t off, ptx::f2& a,
-                                          ptx::f2& b) {
-  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sm + off);
-  a.v = v.x;
-  b.v = v.y;
-}
-
 template <int GP>
 __device__ __forceinline__ void load_q(const uint8_t* sm, uint32_t qrow, ptx::f2 (&qv)[GP]) {
 #pragma unroll
-  for (int g = 0; g + 1 < GP; g += 2) lds_pair2(sm, qrow + 8 * g, qv[g], qv[g + 1]);
+  for (int g = 0; g + 1 < GP; g += 2) {
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(sm + qrow + 8 * g);
+    qv[g].v = v.x;
+    qv[g + 1].v = v.y;
+  }
   if constexpr (GP % 2)
     qv[GP - 1].v = *reinterpret_cast<const unsigned long long*>(sm + qrow + 8 * (GP - 1));
 }
@@ -167,201 +131,207 @@ __device__ __forceinline__ uint32_t read_bits_g(const uint32_t* __restrict__ wor
   return nbits >= 32 ? v : (v & ((1u << nbits) - 1u));
 }
 
-template <int B>
-__device__ __forceinline__ void load_words(uint32_t (&w)[CodeWin<B>::WORDS],
-                                           const uint32_t* __restrict__ row) {
-#pragma unroll
-  for (int i = 0; i < CodeWin<B>::WORDS; ++i) w[i] = __ldg(row + i);
+// compile-time loop: f(std::integral_constant<int, i>) for i < N
+template <typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
-// One code row of the recurrence for the lane's 4 items (prod kept as two
-// packed pairs: items {0,1} and {2,3}).
-template <int B, int GP, bool LUT, bool REPL>
-__device__ __forceinline__ void chain_row(const uint8_t* sm, const uint32_t (&w)[CodeWin<B>::WORDS],
-                                          int sh, uint32_t qrow, uint32_t lut_s, float pstep,
-                                          ptx::f2 (&prod)[2], ptx::f2 (&acc)[4][GP]) {
-  ptx::f2 qv[GP];
-  load_q<GP>(sm, qrow, qv);
-  if constexpr (LUT && lut_group(B) > 1) {
-    // two pair lookups: items {0,1} and {2,3}; lut_s is this lane's copy base
-    constexpr uint32_t STRIDE = REPL ? 128u : 16u;
-    const uint32_t x = (uint32_t)code_window<B>(w, sh);
-    constexpr uint32_t M2 = (1u << (2 * B)) - 1u;
-    uint32_t i0, i1;
-    if constexpr (B == 4) {
-      const uint32_t b0 = (uint32_t)(sh >> 3);
-      i0 = __byte_perm(w[0], 0u, 0x4440u | b0);
-      i1 = __byte_perm(w[0], 0u, 0x4440u | (b0 + 1));
-    } else {
-      i0 = x & M2;
-      i1 = (x >> (2 * B)) & M2;
-    }
-    ptx::f2 cp[2], sp[2];
-    lds_pair2(sm, lut_s + i0 * STRIDE, cp[0], sp[0]);
-    lds_pair2(sm, lut_s + i1 * STRIDE, cp[1], sp[1]);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const ptx::f2 f = ptx::f2_mul(prod[h], cp[h]);
-      ptx::f2_mul_acc(prod[h], sp[h]);
-#pragma unroll
-      for (int g = 0; g < GP; ++g) {
-        ptx::f2_fma_s_acc(ptx::f2_lo(f), qv[g], acc[2 * h][g]);
-        ptx::f2_fma_s_acc(ptx::f2_hi(f), qv[g], acc[2 * h + 1][g]);
-      }
-    }
+// N-bit field at compile-time bit offset S of a register-resident string
+template <int N, int S, int W>
+__device__ __forceinline__ uint32_t field(const uint32_t (&w)[W]) {
+  constexpr int wi = S / 32, sh = S % 32;
+  constexpr uint32_t M = (N >= 32) ? 0xffffffffu : ((1u << N) - 1u);
+  if constexpr (sh + N <= 32) {
+    return (w[wi] >> sh) & M;
   } else {
-    const uint64_t y = code_window<B>(w, sh);
-    float pr[4] = {ptx::f2_lo(prod[0]), ptx::f2_hi(prod[0]), ptx::f2_lo(prod[1]),
-                   ptx::f2_hi(prod[1])};
+    return __funnelshift_r(w[wi], w[wi + 1], sh) & M;
+  }
+}
+// the same field pre-scaled by 2^L (a table byte offset): one shift + one
+// LOP3 that also ORs in the lane's replica offset `orv` (< 2^L)
+template <int N, int S, int L, int W>
+__device__ __forceinline__ uint32_t field_addr(const uint32_t (&w)[W], uint32_t orv) {
+  constexpr int wi = S / 32, sh = S % 32;
+  constexpr uint32_t M = ((1u << N) - 1u) << L;
+  uint32_t x;
+  if constexpr (sh + N > 32) {
+    x = __funnelshift_r(w[wi], w[wi + 1], sh) << L;
+  } else if constexpr (sh >= L) {
+    x = w[wi] >> (sh - L);
+  } else {
+    x = w[wi] << (L - sh);
+  }
+  return (x & M) | orv;
+}
+
+// code string of one item: W words from the WI layout (quad loads)
+template <int W>
+__device__ __forceinline__ void load_item(uint32_t (&w)[W], const uint4* __restrict__ blk4,
+                                          int granule, int lane) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t c = code_at<B>(y, k);
-      float cs, sn;
-      if constexpr (LUT) {
-        const float2 t = lds_f2(sm, lut_s + c * (REPL ? 128u : 8u));
-        cs = t.x;
-        sn = t.y;
-      } else {
-        sincospif((float)c * pstep, &sn, &cs);
-      }
-      const float f = pr[k] * cs;
-#pragma unroll
-      for (int g = 0; g < GP; ++g) ptx::f2_fma_s_acc(f, qv[g], acc[k][g]);
-      pr[k] *= sn;
-    }
-    prod[0] = ptx::f2_make(pr[0], pr[1]);
-    prod[1] = ptx::f2_make(pr[2], pr[3]);
+  for (int q = 0; q < W / 4; ++q) {
+    const uint4 v = __ldg(blk4 + ((size_t)granule * (W / 4) + q) * 32 + lane);
+    w[4 * q] = v.x;
+    w[4 * q + 1] = v.y;
+    w[4 * q + 2] = v.z;
+    w[4 * q + 3] = v.w;
   }
 }
 
-// Logits (base 2) of items sub*TI + 4*lane + k, k < 4, for G heads.
-//   codes : page code block (coordinate-major rows of P*B bits, radius row last)
-//   sm    : the kernel's shared buffer; qs_s / lut_s: byte offsets of the q pairs
-//           [d][GP] (float2) and of this tier's table
-// Code words are requested LA rows ahead of use through a ring of register
-// buffers (no moves of in-flight loads); the look-ahead may read a few rows
-// past the block, which the code pool's tail slack absorbs.
-template <int B, int GP, bool LUT, bool REPL, int PT>
-__device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes, int d, int P_rt,
-                                               int TI, const sphkv_page_t& pg, int sub, int lane,
-                                               const uint8_t* sm, uint32_t qs_s, uint32_t lut_s,
-                                               float lg[4][2 * GP]) {
-  constexpr int NW = CodeWin<B>::WORDS;
-  const int P = PT ? PT : P_rt;  // PT != 0: page size known at compile time (row stride immediates)
-  const int item0 = sub * TI + 4 * lane;
-  const uint32_t* base = reinterpret_cast<const uint32_t*>(codes + pg.code_off);
-  const int row_words = P * B / 32;
-  const uint32_t obit = (uint32_t)item0 * B;
-  const uint32_t* lane_row = base + (obit >> 5);
-  const int sh = (int)(obit & 31);
-  const uint32_t qstride = GP * 8;
-  const float pstep = (float)(1.0 / (double)((1u << B) - 1u));
+// Rows per "period": the smallest row count whose codes fill whole 32-bit
+// words, so every code's bit offset inside a period is a compile-time
+// constant.  WP = words per period.
+template <int B>
+struct Period {
+  static constexpr int R = (B == 1) ? 32 : (B == 2) ? 16 : (B == 4) ? 8 : (B == 8) ? 4
+                         : (B == 16) ? 2 : (B % 4 == 0) ? 8 : (B % 2 == 0) ? 16 : 32;
+  static constexpr int WP = R * B / 32;
+};
 
-  ptx::f2 prod[2] = {ptx::f2_make(1.f, 1.f), ptx::f2_make(1.f, 1.f)};
+// word w (runtime) of tile item k (lane + 32 k): one LDG.32 (L1-resident:
+// the tile's granules are one contiguous block)
+template <int W>
+__device__ __forceinline__ uint32_t item_word(const uint32_t* __restrict__ blk, int sub, int k,
+                                              int lane, int w) {
+  return __ldg(blk + wi_word(sub * 128 + 32 * k + lane, w, W));
+}
+
+// One period (R rows starting at row r0 = per * R) of the feature recurrence
+// for the lane's 4 items, codes in cw[k][0..WP).  MODE 2: row-pair table,
+// 1: single-code table, 0: sincospif.
+template <int B, int GP, int MODE, int STR, int RR = Period<B>::R>
+__device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::WP],
+                                            const uint8_t* sm, uint32_t qrow0, uint32_t tb,
+                                            uint32_t orv, float (&prod)[4],
+                                            ptx::f2 (&acc)[4][GP]) {
+  constexpr int R = Period<B>::R, WP = Period<B>::WP;
+  constexpr uint32_t QR = GP * 8;
+  if constexpr (MODE == 2) {
+    static_assert(RR % 2 == 0, "row pairs");
+    static_for<RR / 2>([&](auto pc) {
+      constexpr int p = decltype(pc)::value;
+      ptx::f2 qa[GP], qb[GP];
+      load_q<GP>(sm, qrow0 + (2 * p) * QR, qa);
+      load_q<GP>(sm, qrow0 + (2 * p + 1) * QR, qb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t a = field_addr<2 * B, 2 * p * B, STR, WP>(cw[k], orv);
+        const float4 e = *reinterpret_cast<const float4*>(sm + tb + a);
+        const ptx::f2 f = ptx::f2_mul(ptx::f2_make(prod[k], prod[k]), ptx::f2_make(e.x, e.y));
+        prod[k] *= e.z;
+#pragma unroll
+        for (int g = 0; g < GP; ++g) {
+          ptx::f2_fma_s_acc(ptx::f2_lo(f), qa[g], acc[k][g]);
+          ptx::f2_fma_s_acc(ptx::f2_hi(f), qb[g], acc[k][g]);
+        }
+      }
+    });
+  } else {
+    const float pstep = (float)(1.0 / (double)((1u << B) - 1u));
+    const float pang = (float)(kPi / (double)((1u << B) - 1u));
+    static_for<RR>([&](auto jc) {
+      constexpr int j = decltype(jc)::value;
+      ptx::f2 qa[GP];
+      load_q<GP>(sm, qrow0 + j * QR, qa);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float cs, sn;
+        if constexpr (MODE == 1) {
+          const uint32_t a = field_addr<B, j * B, STR, WP>(cw[k], orv);
+          const float2 t = *reinterpret_cast<const float2*>(sm + tb + a);
+          cs = t.x;
+          sn = t.y;
+        } else if constexpr (MODE == 3) {
+          // MUFU sin/cos (no shared-memory traffic): code -> float exactly via
+          // the 2^23 magic, angle = code * step in fp32 (abs err ~2e-7)
+          const float x = __uint_as_float(0x4B000000u | field<B, j * B, WP>(cw[k])) - 8388608.f;
+          __sincosf(x * pang, &sn, &cs);
+        } else {
+          sincospif((float)field<B, j * B, WP>(cw[k]) * pstep, &sn, &cs);
+        }
+        const float f = prod[k] * cs;
+        prod[k] *= sn;
+#pragma unroll
+        for (int g = 0; g < GP; ++g) ptx::f2_fma_s_acc(f, qa[g], acc[k][g]);
+      }
+    });
+  }
+}
+
+// Specialised tile (B, D known).  A runtime loop over whole periods (codes
+// of the next period requested while the current one is computed), then the
+// remaining polar rows and the circular row with runtime extraction.
+template <int B, int D, int GP, int MODE, bool REPL>
+__device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int sub, int lane,
+                                         const uint8_t* sm, uint32_t qs, uint32_t tb,
+                                         uint32_t rbit0, int rb, float rscale,
+                                         float lg[4][2 * GP]) {
+  constexpr int W = item_words(D, B);
+  constexpr int R = Period<B>::R, WP = Period<B>::WP;
+  constexpr int NP = D - 2;      // polar rows
+  constexpr int NFULL = NP / R;  // whole periods of polar rows
+  constexpr int EB = (MODE == 2) ? 16 : 8;
+  constexpr int STR = REPL ? 7 : ((MODE == 2) ? 4 : 3);
+  constexpr uint32_t QR = GP * 8;
+  const uint32_t orv = REPL ? (uint32_t)(lane % (128 / EB)) * EB : 0u;
+  const uint32_t* blk = reinterpret_cast<const uint32_t*>(blkb);
+  float prod[4];
   ptx::f2 acc[4][GP];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    prod[k] = 1.f;
+#pragma unroll
+    for (int g = 0; g < GP; ++g) acc[k][g] = ptx::f2_make(0.f, 0.f);
+  }
+  uint32_t cw[4][WP];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int g = 0; g < GP; ++g) acc[k][g] = ptx::f2_make(0.f, 0.f);
-
-#if SPHKV_RING
-  // ring of LA+1 word buffers: row j+LA is requested while row j is consumed;
-  // the unroll by LA+1 makes every buffer index a compile-time constant.
-#ifndef SPHKV_LA
-#define SPHKV_LA 6
-#endif
-  constexpr int LA = SPHKV_LA;
-  uint32_t wb[LA + 1][NW];
+    for (int i = 0; i < WP; ++i) cw[k][i] = item_word<W>(blk, sub, k, lane, i);
+#pragma unroll 1
+  for (int per = 0; per < NFULL; ++per) {
+    uint32_t nw[4][WP];
+    const int wn = (per + 1) * WP;  // next period's first word (< W: a tail follows)
 #pragma unroll
-  for (int u = 0; u < LA; ++u) load_words<B>(wb[u], lane_row + u * row_words);
-  const int nrow = d - 2;
-  const uint32_t* next = lane_row + LA * row_words;
-  uint32_t qrow = qs_s;
-  int j = 0;
-  for (; j + (LA + 1) <= nrow; j += LA + 1) {
+    for (int k = 0; k < 4; ++k)
 #pragma unroll
-    for (int u = 0; u <= LA; ++u) {
-      load_words<B>(wb[(u + LA) % (LA + 1)], next + u * row_words);  // may run past row d-1: pool has slack
-      chain_row<B, GP, LUT, REPL>(sm, wb[u], sh, qrow + u * qstride, lut_s, pstep, prod, acc);
-    }
-    next += (LA + 1) * row_words;
-    qrow += (LA + 1) * qstride;
+      for (int i = 0; i < WP; ++i) nw[k][i] = item_word<W>(blk, sub, k, lane, min(wn + i, W - 1));
+    period_rows<B, GP, MODE, STR>(cw, sm, qs + per * R * QR, tb, orv, prod, acc);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < WP; ++i) cw[k][i] = nw[k][i];
   }
-  // tail: wb[u] holds row j+u for u < LA; r = nrow - j < LA+1 polar rows remain
-  const int r = nrow - j;
-  if (r == LA) load_words<B>(wb[LA], next);
-#pragma unroll
-  for (int u = 0; u < LA; ++u)
-    if (u < r) chain_row<B, GP, LUT, REPL>(sm, wb[u], sh, qrow + u * qstride, lut_s, pstep, prod, acc);
-  uint32_t w0[NW];
-#pragma unroll
-  for (int u = 0; u <= LA; ++u) {
-    if (u == r) {
-#pragma unroll
-      for (int i = 0; i < NW; ++i) w0[i] = wb[u][i];
-    }
-  }
-#else
-  uint32_t w0[NW], w1[NW], w2[NW];
-  load_words<B>(w0, lane_row);
-  load_words<B>(w1, lane_row + row_words);
-  const int nrow = d - 2;
-  const uint32_t* next = lane_row + 2 * row_words;
-  uint32_t qrow = qs_s;
-  int j = 0;
-  for (; j + 3 <= nrow; j += 3) {
-    load_words<B>(w2, next);
-    chain_row<B, GP, LUT, REPL>(sm, w0, sh, qrow, lut_s, pstep, prod, acc);
-    load_words<B>(w0, next + row_words);
-    chain_row<B, GP, LUT, REPL>(sm, w1, sh, qrow + qstride, lut_s, pstep, prod, acc);
-    load_words<B>(w1, next + 2 * row_words);
-    chain_row<B, GP, LUT, REPL>(sm, w2, sh, qrow + 2 * qstride, lut_s, pstep, prod, acc);
-    next += 3 * row_words;
-    qrow += 3 * qstride;
-  }
-  const int rem = nrow - j;
-  if (rem >= 1) {
-    chain_row<B, GP, LUT, REPL>(sm, w0, sh, qrow, lut_s, pstep, prod, acc);
-    qrow += qstride;
-    if (rem == 2) {
-      load_words<B>(w2, next);
-      chain_row<B, GP, LUT, REPL>(sm, w1, sh, qrow, lut_s, pstep, prod, acc);
-#pragma unroll
-      for (int i = 0; i < NW; ++i) w0[i] = w2[i];
-    } else {
-#pragma unroll
-      for (int i = 0; i < NW; ++i) w0[i] = w1[i];
-    }
-  }
-#endif
-  // circular last angle (row d-2, now in w0): step 2*pi/2^B -> sincospi(code * 2^(1-B))
-  const float pf[4] = {ptx::f2_lo(prod[0]), ptx::f2_hi(prod[0]), ptx::f2_lo(prod[1]),
-                       ptx::f2_hi(prod[1])};
+  // last partial period (compile-time row count), then the circular row
+  // NP = D-2, whose code lies in the same period window
+  constexpr int RR = NP - NFULL * R;
+  if constexpr (RR > 0)
+    period_rows<B, GP, MODE, STR, RR>(cw, sm, qs + NFULL * R * QR, tb, orv, prod, acc);
   {
-    const uint64_t y = code_window<B>(w0, sh);
     ptx::f2 qa[GP], qb[GP];
-    load_q<GP>(sm, qs_s + (d - 2) * qstride, qa);
-    load_q<GP>(sm, qs_s + (d - 1) * qstride, qb);
-    const float cstep = ldexpf(1.0f, 1 - B);
+    load_q<GP>(sm, qs + NP * QR, qa);
+    load_q<GP>(sm, qs + (NP + 1) * QR, qb);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       float sn, cs;
-      sincospif((float)code_at<B>(y, k) * cstep, &sn, &cs);
-      const float f0 = pf[k] * cs, f1 = pf[k] * sn;
+      sincospif((float)field<B, RR * B, WP>(cw[k]) * (1.0f / (float)(1u << (B - 1))), &sn, &cs);
+      const float f0 = prod[k] * cs, f1 = prod[k] * sn;
 #pragma unroll
       for (int g = 0; g < GP; ++g) {
-        acc[k][g] = ptx::f2_fma_s(f0, qa[g], acc[k][g]);
-        acc[k][g] = ptx::f2_fma_s(f1, qb[g], acc[k][g]);
+        ptx::f2_fma_s_acc(f0, qa[g], acc[k][g]);
+        ptx::f2_fma_s_acc(f1, qb[g], acc[k][g]);
       }
     }
   }
-  // decoded radii r~ = code * (scale / levels)  (row d-1 holds the radius stream)
-  const uint64_t rbit0 = (uint64_t)(d - 1) * P * B;
-  const int rb = pg.rbits;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    const uint32_t rc = read_bits_g(base, rbit0 + (uint64_t)(item0 + k) * rb, rb);
-    const float rr = (float)rc * pg.rscale;
+    const uint32_t rc = read_bits_g(blk, rbit0 + (uint64_t)(sub * 128 + 32 * k + lane) * rb, rb);
+    const float rr = (float)rc * rscale;
 #pragma unroll
     for (int g = 0; g < GP; ++g) {
       lg[k][2 * g] = rr * ptx::f2_lo(acc[k][g]);
@@ -370,40 +340,126 @@ __device__ __forceinline__ void ada_logit_tile(const uint8_t* __restrict__ codes
   }
 }
 
+// Generic tile (any B <= 16, any d): runtime loops, words fetched per row
+// from global memory; same math (row-pair table rows in pairs, single table,
+// or sincospif).
 template <int GP>
-__device__ void ada_logit_dispatch(int B, const uint8_t* codes, int d, int P, int TI,
-                                   const sphkv_page_t& pg, int sub, int lane, const uint8_t* sm,
-                                   uint32_t qs_s, int lut_enc, float lg[4][2 * GP]) {
-  // lut_enc: (byte offset << 1) | replicated, or -1 (no table: sincospi)
-  const bool has = lut_enc >= 0;
-  const bool repl = has && (lut_enc & 1);
-  const uint32_t base = has ? (uint32_t)(lut_enc >> 1) : 0u;
-  switch (B) {
-#define SPHKV_TILE(b, L, R, PP)                                                              \
-  ada_logit_tile<b, GP, L, R, PP>(codes, d, P, TI, pg, sub, lane, sm, qs_s,                 \
-                                  base + (R ? (uint32_t)(lane % lut_rep(b)) * lut_entry_bytes(b) \
-                                            : 0u), lg)
-#define SPHKV_CASE(b)                                                                        \
-  case b:                                                                                    \
-    if (b <= LUT_MAX_BITS && has) {                                                          \
-      if (repl) {                                                                            \
-        if (P == 256) SPHKV_TILE(b, (b <= LUT_MAX_BITS), true, 256);                         \
-        else SPHKV_TILE(b, (b <= LUT_MAX_BITS), true, 0);                                    \
-      } else {                                                                               \
-        if (P == 256) SPHKV_TILE(b, (b <= LUT_MAX_BITS), false, 256);                        \
-        else SPHKV_TILE(b, (b <= LUT_MAX_BITS), false, 0);                                   \
-      }                                                                                      \
-    } else {                                                                                 \
-      SPHKV_TILE(b, false, false, 0);                                                        \
-    }                                                                                        \
-    break;
-    SPHKV_CASE(1) SPHKV_CASE(2) SPHKV_CASE(3) SPHKV_CASE(4) SPHKV_CASE(5) SPHKV_CASE(6)
-    SPHKV_CASE(7) SPHKV_CASE(8) SPHKV_CASE(9) SPHKV_CASE(10) SPHKV_CASE(11) SPHKV_CASE(12)
-    SPHKV_CASE(13) SPHKV_CASE(14) SPHKV_CASE(15) SPHKV_CASE(16)
-#undef SPHKV_CASE
-#undef SPHKV_TILE
-    default: break;
+__device__ __noinline__ void ada_tile_generic(const uint8_t* __restrict__ blk, int B, int d,
+                                              int P, int sub, int lane, const uint8_t* sm, uint32_t qs,
+                                              int lut_enc, uint32_t rbit0, int rb, float rscale,
+                                              float lg[4][2 * GP]) {
+  const int W = item_words(d, B);
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(blk);
+  const bool has = lut_enc >= 0, repl = has && (lut_enc & 1);
+  const int grp = lut_group(B), eb = lut_entry_bytes(B);
+  const uint32_t tbase = has ? (uint32_t)(lut_enc >> 1) + (repl ? (lane % lut_rep(B)) * eb : 0) : 0;
+  const uint32_t stride = repl ? 128u : (uint32_t)eb;
+  const uint32_t QR = GP * 8;
+  const float pstep = (float)(1.0 / (double)((1u << B) - 1u));
+  for (int kk = 0; kk < 4; ++kk) {
+    const int item = sub * 128 + 32 * kk + lane;
+    if (item >= P) {  // beyond a narrow page: masked by the caller
+      for (int g = 0; g < 2 * GP; ++g) lg[kk][g] = 0.f;
+      continue;
+    }
+    auto code = [&](int bit, int n) -> uint32_t {
+      const int w0 = bit >> 5, sh = bit & 31;
+      const uint32_t lo = __ldg(words + wi_word(item, w0, W));
+      const uint32_t hi = (sh + n > 32) ? __ldg(words + wi_word(item, w0 + 1, W)) : 0u;
+      return __funnelshift_r(lo, hi, sh) & ((1u << n) - 1u);
+    };
+    float prod = 1.f;
+    ptx::f2 acc[GP];
+    for (int g = 0; g < GP; ++g) acc[g] = ptx::f2_make(0.f, 0.f);
+    int j = 0;
+    if (has && grp == 2) {
+      for (; j + 1 < d - 2; j += 2) {
+        const float4 e = *reinterpret_cast<const float4*>(sm + tbase + code(j * B, 2 * B) * stride);
+        ptx::f2 qa[GP], qb[GP];
+        load_q<GP>(sm, qs + j * QR, qa);
+        load_q<GP>(sm, qs + (j + 1) * QR, qb);
+        const float f0 = prod * e.x, f1 = prod * e.y;
+        prod *= e.z;
+        for (int g = 0; g < GP; ++g) {
+          ptx::f2_fma_s_acc(f0, qa[g], acc[g]);
+          ptx::f2_fma_s_acc(f1, qb[g], acc[g]);
+        }
+      }
+    }
+    for (; j < d - 2; ++j) {
+      float cs, sn;
+      const uint32_t c = code(j * B, B);
+      if (has && grp == 1) {
+        const float2 t = *reinterpret_cast<const float2*>(sm + tbase + c * stride);
+        cs = t.x;
+        sn = t.y;
+      } else {
+        sincospif((float)c * pstep, &sn, &cs);
+      }
+      ptx::f2 qa[GP];
+      load_q<GP>(sm, qs + j * QR, qa);
+      const float f = prod * cs;
+      prod *= sn;
+      for (int g = 0; g < GP; ++g) ptx::f2_fma_s_acc(f, qa[g], acc[g]);
+    }
+    {
+      float sn, cs;
+      sincospif((float)code((d - 2) * B, B) * (1.0f / (float)(1u << (B - 1))), &sn, &cs);
+      ptx::f2 qa[GP], qb[GP];
+      load_q<GP>(sm, qs + (d - 2) * QR, qa);
+      load_q<GP>(sm, qs + (d - 1) * QR, qb);
+      const float f0 = prod * cs, f1 = prod * sn;
+      for (int g = 0; g < GP; ++g) {
+        ptx::f2_fma_s_acc(f0, qa[g], acc[g]);
+        ptx::f2_fma_s_acc(f1, qb[g], acc[g]);
+      }
+    }
+    const uint32_t rc = read_bits_g(words, rbit0 + (uint64_t)item * rb, rb);
+    const float rr = (float)rc * rscale;
+    for (int g = 0; g < GP; ++g) {
+      lg[kk][2 * g] = rr * ptx::f2_lo(acc[g]);
+      lg[kk][2 * g + 1] = rr * ptx::f2_hi(acc[g]);
+    }
   }
+}
+
+// Logits (base 2) of the tile's items sub*128 + 32 k + lane, k < 4, G heads.
+// lut_enc: (table byte offset << 1) | replicated, or -1 (no table).
+template <int GP>
+__device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, int d, int P,
+                                                   const sphkv_page_t& pg, int sub, int lane,
+                                                   const uint8_t* sm, uint32_t qs, int lut_enc,
+                                                   float lg[4][2 * GP]) {
+  const uint8_t* blk = codes + pg.code_off;
+  const uint32_t rbit0 = (uint32_t)(angle_part_bytes(d, P, B) * 8);
+  const int rb = pg.rbits;
+  const float rs = pg.rscale;
+  const bool has = lut_enc >= 0, repl = has && (lut_enc & 1);
+  const uint32_t tb = has ? (uint32_t)(lut_enc >> 1) : 0u;
+#define SPHKV_WI(b, dd, mode, rp) \
+  ada_tile_wi<b, dd, GP, mode, rp>(blk, sub, lane, sm, qs, tb, rbit0, rb, rs, lg)
+  if (P % 128 != 0) {
+    // pages narrower than a tile: generic path (guards items >= P)
+  } else if (d == 128) {
+    if (B == 2 && has && repl) { SPHKV_WI(2, 128, 2, true); return; }
+    if (B == 4 && has && repl) { SPHKV_WI(4, 128, 2, true); return; }
+    if (B == 4 && has && !repl) { SPHKV_WI(4, 128, 2, false); return; }
+    if (B == 6 && has && repl) { SPHKV_WI(6, 128, 1, true); return; }
+    if (B == 7 && has && repl) { SPHKV_WI(7, 128, 1, true); return; }
+#ifdef SPHKV_MUFU12
+    if (B == 12) { SPHKV_WI(12, 128, 3, false); return; }
+#endif
+    if (B == 12 && has && !repl) { SPHKV_WI(12, 128, 1, false); return; }
+    if (B == 15 && !has) { SPHKV_WI(15, 128, 0, false); return; }
+  } else if (d == 64) {
+    if (B == 2 && has && repl) { SPHKV_WI(2, 64, 2, true); return; }
+    if (B == 4 && has && repl) { SPHKV_WI(4, 64, 2, true); return; }
+    if (B == 6 && has && repl) { SPHKV_WI(6, 64, 1, true); return; }
+    if (B == 7 && has && repl) { SPHKV_WI(7, 64, 1, true); return; }
+    if (B == 12 && has && !repl) { SPHKV_WI(12, 64, 1, false); return; }
+  }
+#undef SPHKV_WI
+  ada_tile_generic<GP>(blk, B, d, P, sub, lane, sm, qs, lut_enc, rbit0, rb, rs, lg);
 }
 
 }  // namespace sphkv

@@ -43,14 +43,31 @@ constexpr int SM_COUNT = 148;
 
 __host__ __device__ inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-// Bytes of one page's code block: (d-1) angle rows + 1 radius row, 16-B padded.
-__host__ __device__ inline uint64_t code_block_bytes(int d, int P, int abits, int rbits) {
-  uint64_t bits = (uint64_t)(d - 1) * P * abits + (uint64_t)P * rbits;
-  uint64_t bytes = (bits + 7) / 8;
-  return (bytes + 15) & ~uint64_t(15);
+// Device angle-code layout of a page: "word-interleaved, item-major" (WI).
+// Item i's d-1 angle codes form one LSB-first bit string (code j at bits
+// [j*b, j*b+b)), padded to W words, W = ceil((d-1)*b/32) rounded up to a
+// multiple of 4.  Items are grouped in granules of 32 and the string is cut
+// into 16-byte quads; quad w4 of item i lives at quad index
+//   ((i / 32) * (W / 4) + w4) * 32 + (i % 32)
+// so lane l of a warp loading quad w4 of items 32t..32t+31 issues one fully
+// coalesced 512-byte LDG.128, and each lane ends up holding its own item's
+// whole code string in registers.  The radius codes follow as one LSB-first
+// row of P*rb bits (the reference radius stream, store.py:205-211).  Export
+// (sphkv_export_streams) converts back to the reference's coordinate-major
+// SoA stream bit for bit.
+__host__ __device__ constexpr int item_words(int d, int abits) {
+  return ((((d - 1) * abits + 31) / 32) + 3) / 4 * 4;
 }
-__host__ __device__ inline uint64_t angle_row_bytes(int P, int abits) {
-  return (uint64_t)P * abits / 8;  // P is a multiple of 32
+__host__ __device__ inline uint64_t angle_part_bytes(int d, int P, int abits) {
+  return (uint64_t)((P + 31) / 32) * item_words(d, abits) * 128;
+}
+__host__ __device__ inline uint64_t code_block_bytes(int d, int P, int abits, int rbits) {
+  const uint64_t rbytes = ((uint64_t)P * rbits + 7) / 8;
+  return angle_part_bytes(d, P, abits) + ((rbytes + 15) & ~uint64_t(15));
+}
+// word index (uint32 units from the block start) of string word w of item i
+__host__ __device__ inline uint64_t wi_word(int i, int w, int W) {
+  return (((uint64_t)(i >> 5) * (W >> 2) + (w >> 2)) * 32 + (i & 31)) * 4 + (w & 3);
 }
 
 // Value-pool element offset (in fp16 elements) of (item i, column e) inside a

@@ -36,12 +36,15 @@ constexpr int ADA_TI = 128;        // items per tile (4 per lane)
 #define SPHKV_NS 12
 #endif
 constexpr int ADA_NS = SPHKV_NS;   // P slots
-constexpr int ADA_NV = 3;          // V slots
-#ifndef SPHKV_PF_MODE
-#define SPHKV_PF_MODE 0
+#ifndef SPHKV_NV
+#define SPHKV_NV 3
 #endif
-#ifndef SPHKV_PF_ROUNDS
-#define SPHKV_PF_ROUNDS 2
+constexpr int ADA_NV = SPHKV_NV;   // V slots
+#ifndef SPHKV_PF_DIST
+#define SPHKV_PF_DIST 8   // L2 prefetch distance in tiles (claim order)
+#endif
+#ifndef SPHKV_PF_V
+#define SPHKV_PF_V 0      // also prefetch each tile's V block to L2 (measured: slower)
 #endif
 #ifndef SPHKV_NPV
 #define SPHKV_NPV 1
@@ -139,34 +142,31 @@ __device__ int build_tiles(const sphkv_store_t& st, const sphkv_unit_t& u, int T
   return nt;
 }
 
-// Write the fp16 weights of one tile (4 items x G per lane) + tile max/sum.
+// Write the fp16 weights of one tile + tile max/sum.  Lane l holds items
+// l + 32 k (k < 4) of the tile; bit k of `valid` says whether item l + 32 k
+// exists.
 template <int NG>
 __device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int prows, int TI,
                                             int lane, int G, const float lg[4][NG],
-                                            int nvalid_lane) {
+                                            uint32_t valid) {
   float* hdr = reinterpret_cast<float*>(slot + prows * prow_bytes);
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
     float m = -INFINITY;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (k < nvalid_lane) m = fmaxf(m, lg[k][g]);
+      if (valid & (1u << k)) m = fmaxf(m, lg[k][g]);
     m = warp_max(m);
-    float pv[4], s = 0.f;
+    float s = 0.f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      float e = (k < nvalid_lane) ? exp2f(lg[k][g] - m) : 0.f;
-      __half h = __float2half_rn(e);
-      pv[k] = __half2float(h);
-      s += pv[k];
+      const float e = (valid & (1u << k)) ? exp2f(lg[k][g] - m) : 0.f;
+      const __half h = __float2half_rn(e);
+      s += __half2float(h);
+      if (g < G && 32 * k + lane < TI)
+        *reinterpret_cast<__half*>(slot + g * prow_bytes + (32 * k + lane) * 2) = h;
     }
     s = warp_sum(s);
-    if (g < G && 4 * lane < TI) {
-      uint2 packed;
-      packed.x = ptx::pack_half2(pv[0], pv[1]);
-      packed.y = ptx::pack_half2(pv[2], pv[3]);
-      *reinterpret_cast<uint2*>(slot + g * prow_bytes + (4 * lane) * 2) = packed;
-    }
     if (lane == 0 && g < 8) {
       hdr[g] = m;
       hdr[8 + g] = s;
@@ -223,6 +223,57 @@ __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, c
         ptx::ldsm_x4_trans(vbase + (item * dvp + sw * 8) * 2, a0, a1, a2, a3);
         ptx::mma_f16(c[i], a0, a1, a2, a3, b0, b1);
       }
+    }
+  }
+  const float* hdr = reinterpret_cast<const float*>(pslot + prows * prow_bytes);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int g = 2 * (lane & 3) + h;
+    const float mt_ = (g < G) ? hdr[g] : 0.f;
+    const float lt = (g < G) ? hdr[8 + g] : 0.f;
+    const float mn = fmaxf(s.m[h], mt_);
+    const float al = exp2f(s.m[h] - mn), be = exp2f(mt_ - mn);
+    s.m[h] = mn;
+    s.l[h] = s.l[h] * al + lt * be;
+#pragma unroll
+    for (int i = 0; i < MTW; ++i) {
+      s.acc[i][h] = s.acc[i][h] * al + c[i][h] * be;
+      s.acc[i][2 + h] = s.acc[i][2 + h] * al + c[i][2 + h] * be;
+    }
+  }
+}
+
+// Fast path of pv_tile for d_v = 128 (16 swizzled chunks per V row), a
+// 128-item tile and all of the warp's m-tiles present: fully unrolled, every
+// ldmatrix address is a per-lane base + an immediate (the XOR swizzle term
+// only depends on the row inside the 8-row group, not on the k-step).
+template <int MTW>
+__device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslot,
+                                            const uint8_t* vslot, int prow_bytes, int prows,
+                                            int mt0, int G, int lane) {
+  float c[MTW][4];
+#pragma unroll
+  for (int i = 0; i < MTW; ++i)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) c[i][r] = 0.f;
+  const int r = lane & 7, mat = lane >> 3;
+  const uint32_t pb = ptx::smem_u32(pslot) + ((lane & 7) & (prows - 1)) * prow_bytes +
+                      ((lane >> 3) & 1) * 16;
+  uint32_t va[MTW];
+#pragma unroll
+  for (int i = 0; i < MTW; ++i) {
+    const int chunk = 2 * (mt0 + i) + (mat & 1);
+    va[i] = ptx::smem_u32(vslot) + ((r + (mat >> 1) * 8) * 128 + (chunk ^ r) * 8) * 2;
+  }
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    uint32_t b0, b1;
+    ptx::ldsm_x2(pb + ks * 32, b0, b1);
+#pragma unroll
+    for (int i = 0; i < MTW; ++i) {
+      uint32_t a0, a1, a2, a3;
+      ptx::ldsm_x4_trans(va[i] + ks * 4096, a0, a1, a2, a3);
+      ptx::mma_f16(c[i], a0, a1, a2, a3, b0, b1);
     }
   }
   const float* hdr = reinterpret_cast<const float*>(pslot + prows * prow_bytes);
@@ -430,56 +481,69 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       }
       // tiles are claimed dynamically (smem counter) to balance the warps;
       // the P slot of tile k is k % NS whoever computes it.
-      const uint64_t ppol = ptx::policy_evict_last();
-      // L2 prefetch of a page's code block (one per page, at its sub-0 tile):
-      // SPHKV_PF_MODE 0 = one bulk prefetch by lane 0, 1 = per-line prefetch by
-      // the whole warp (evict_last either way)
+      // L2 prefetch, PF_DIST tiles ahead of the claim order: the tile's code
+      // granules (contiguous in the WI layout), its radius row with the
+      // page's first tile, and (SPHKV_PF_V) its fp16 V block, so the V bulk
+      // copy and the code loads hit L2 and many more bytes are in flight per
+      // SM than the smem rings alone could hold.
       auto prefetch_tile = [&](int t) {
-        if (t < nt) {
+        if (t < nt && lane == 0) {
           const TileEntry tn = tiles[t];
-          if ((tn.sub_off >> 24) == 0) {
-            const sphkv_page_t pn = st.pages[tn.page];
-            const uint32_t bytes = (uint32_t)code_block_bytes(d, P, pn.abits, pn.rbits);
-#if SPHKV_PF_MODE == 0
-            if (lane == 0) ptx::bulk_prefetch_l2_hint(st.codes + pn.code_off, bytes, ppol);
-#else
-            for (uint32_t o = lane * 128u; o < bytes; o += 32u * 128u)
-              ptx::prefetch_l2_line(st.codes + pn.code_off + o);
-#endif
+          const int sb = tn.sub_off >> 24;
+          const sphkv_page_t pn = st.pages[tn.page];
+          const uint64_t W4 = (uint64_t)item_words(d, pn.abits) * 128;  // bytes per granule
+          const int g0 = sb * TI / 32, ng = (TI + 31) / 32;
+          ptx::bulk_prefetch_l2(st.codes + pn.code_off + g0 * W4, (uint32_t)(ng * W4));
+          if (sb == 0) {
+            const uint64_t ab = angle_part_bytes(d, P, pn.abits);
+            ptx::bulk_prefetch_l2(st.codes + pn.code_off + ab,
+                                  (uint32_t)(code_block_bytes(d, P, pn.abits, pn.rbits) - ab));
           }
+#if SPHKV_PF_V
+          ptx::bulk_prefetch_l2(st.values + ((size_t)tn.page * P + (size_t)sb * TI) * dvp, vbytes);
+#endif
         }
       };
 #pragma unroll 1
-      for (int r = 0; r < SPHKV_PF_ROUNDS; ++r) prefetch_tile(warp + r * ADA_NL);
+      for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t);
       for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(tile_ctr, 1);
         k = __shfl_sync(0xffffffffu, k, 0);
         if (k >= nt) break;
-        prefetch_tile(k + SPHKV_PF_ROUNDS * ADA_NL);
+        prefetch_tile(k + SPHKV_PF_DIST);
         const uint32_t gk = gbase + k;
         const TileEntry te = tiles[k];
         const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
         const sphkv_page_t pg = st.pages[te.page];
         const int ti = tier_index(st, pg.tier);
         float lg[4][2 * GP];  // LUT region starts at smem[0]
-        ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, TI, pg, sub, lane, smem, p.smem_q,
+#ifdef SPHKV_DBG_NOLOGIT  // bottleneck probe: skip the logit math
+        for (int a_ = 0; a_ < 4; ++a_)
+          for (int b_ = 0; b_ < 2 * GP; ++b_) lg[a_][b_] = (float)(a_ + b_) * 0.01f + (float)ti;
+#else
+        ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
                                p.lut_off[ti], lg);
-        int nvalid = pg.count - sub * TI - 4 * lane;
-        nvalid = nvalid < 0 ? 0 : (nvalid > 4 ? 4 : nvalid);
-        if (4 * lane >= TI) nvalid = 0;
-        if (p.logits_dbg != nullptr) {
-          float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 4 * lane) * p.G;
+#endif
+        uint32_t valid = 0;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
+        for (int kk = 0; kk < 4; ++kk) {
+          const int it = sub * TI + 32 * kk + lane;
+          if (32 * kk + lane < TI && it < pg.count) valid |= 1u << kk;
+        }
+        if (p.logits_dbg != nullptr) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 32 * kk + lane) * p.G;
 #pragma unroll
             for (int g = 0; g < 2 * GP; ++g)
-              if (kk < nvalid && g < p.G) dst[kk * p.G + g] = lg[kk][g] * (1.0f / kLog2e);
+              if ((valid & (1u << kk)) && g < p.G) dst[g] = lg[kk][g] * (1.0f / kLog2e);
+          }
         }
         const int ps = gk % ADA_NS;
         ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
         write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, p.prows, TI, lane, p.G, lg,
-                            nvalid);
+                            valid);
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
       }
@@ -508,13 +572,20 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k);
       PVState<ADA_MTW> s;
       pv_init(s);
+      const bool fast_pv = (dvp == 128 && TI == 128 && mtn == ADA_MTW);
       for (int k = 0; k < nt; ++k) {
         const uint32_t gk = gbase + k;
         const int vs = gk % ADA_NV, ps = gk % ADA_NS;
         ptx::mbar_wait(&v_full[vs], (gk / ADA_NV) & 1);
         ptx::mbar_wait(&p_full[ps], (gk / ADA_NS) & 1);
-        pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
-                         p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane);
+#ifndef SPHKV_DBG_NOPV  // bottleneck probe: skip the P.V math
+        if (fast_pv)
+          pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                               p.prow_bytes, p.prows, mt0, p.G, lane);
+        else
+          pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                           p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane);
+#endif
         __syncwarp();
         if (lane == 0) {
           ptx::mbar_arrive(&p_empty[ps]);

@@ -335,12 +335,27 @@ __global__ void k_pack_write(sphkv_store_t st, int first_page, int n_pages, int 
   const int idx = valid ? page_items[(int64_t)(pid - first_page) * P + slot] : 0;
   const double r = valid ? radii[idx] : 0.0;
   uint32_t* block = reinterpret_cast<uint32_t*>(st.codes + pg.code_off);
-  const int row_words = P * b / 32;
+  const int W = item_words(d, b);
   const double ps = polar_step(b), cs = circular_step(b);
+  // Codes arrive in descending row order (circular d-2, then polar d-3..0),
+  // so the lane assembles its item string word by word from the top and
+  // stores each finished word once (coalesced across the warp's 32 items).
+  uint32_t acc = 0;
+  int cur = W - 1;
+  auto put_word = [&](int w, uint32_t v) {
+    while (cur > w) {
+      block[wi_word(slot, cur, W)] = acc;
+      acc = 0;
+      --cur;
+    }
+    acc |= v;
+  };
   auto emit = [&](int j, double a) {
     uint32_t c = 0;
     if (valid) c = (j == d - 2) ? quant_circ(a, cs, b) : quant_polar(a, ps, b);
-    warp_store_bits(wbuf, block + (size_t)j * row_words + chunk * b, c, b, lane);
+    const int bit = j * b, w = bit >> 5, sh = bit & 31;
+    if (sh + b > 32) put_word(w + 1, c >> (32 - sh));
+    put_word(w, c << sh);
   };
   if (angles != nullptr) {
     const double* ar = angles + (int64_t)idx * (d - 1);
@@ -352,7 +367,8 @@ __global__ void k_pack_write(sphkv_store_t st, int first_page, int n_pages, int 
     double rr = valid ? r : 0.0;
     encode_desc(keys + (int64_t)idx * d, d, rr, emit);
   }
-  // radius row
+  put_word(-1, 0u);  // flush word 0 (and any untouched padding words above)
+  // radius row (SoA, LSB-first) after the angle part
   {
     const double levels = (double)((1u << rb) - 1u);
     uint32_t c = 0;
@@ -361,7 +377,8 @@ __global__ void k_pack_write(sphkv_store_t st, int first_page, int n_pages, int 
       x = fmin(fmax(x, 0.0), 1.0);
       c = (uint32_t)rint(__dmul_rn(x, levels));
     }
-    warp_store_bits(wbuf, block + (size_t)(d - 1) * row_words + chunk * rb, c, rb, lane);
+    uint32_t* rrow = block + angle_part_bytes(d, P, b) / 4;
+    warp_store_bits(wbuf, rrow + chunk * rb, c, rb, lane);
   }
   // values (swizzled, zero padded), protect, token id
   const int dv = st.d_v, dvp = (dv + 15) / 16 * 16;
@@ -506,21 +523,22 @@ __global__ void k_append_write(sphkv_store_t st, int n, const int16_t* __restric
   uint32_t* words = reinterpret_cast<uint32_t*>(blk);
   const double* ang = ws.angles + (int64_t)g * (d - 1);
   const double ps = polar_step(b), cs = circular_step(b);
-  auto put = [&](uint64_t bit, uint32_t code, int nb) {
-    uint64_t w = bit >> 5;
-    int sh = (int)(bit & 31);
-    words[w] |= code << sh;
-    if (sh + nb > 32) words[w + 1] |= code >> (32 - sh);
-  };
+  const int W = item_words(d, b);
+  // lanes write different codes of the same item string: OR atomically
   for (int j = lane; j < d - 1; j += 32) {
     uint32_t c = (j == d - 2) ? quant_circ(ang[j], cs, b) : quant_polar(ang[j], ps, b);
-    put(((uint64_t)j * P + pos) * b, c, b);
+    const int bit = j * b, w = bit >> 5, sh = bit & 31;
+    atomicOr(words + wi_word(pos, w, W), c << sh);
+    if (sh + b > 32) atomicOr(words + wi_word(pos, w + 1, W), c >> (32 - sh));
   }
   if (lane == 0) {
     // quantize_radius: Python round() == round-half-even (codec.py:353-355)
     double x = fmin(fmax(__ddiv_rn(ws.radius[g], pg.radius_scale), 0.0), 1.0);
     uint32_t rc = (uint32_t)rint(__dmul_rn(x, (double)((1u << rb) - 1u)));
-    put((uint64_t)(d - 1) * P * b + (uint64_t)pos * rb, rc, rb);
+    const uint64_t bit = angle_part_bytes(d, P, b) * 8 + (uint64_t)pos * rb;
+    const int sh = (int)(bit & 31);
+    atomicOr(words + (bit >> 5), rc << sh);
+    if (sh + rb > 32) atomicOr(words + (bit >> 5) + 1, rc >> (32 - sh));
   }
   const int dv = st.d_v, dvp = (dv + 15) / 16 * 16;
   uint16_t* vrow = st.values + (int64_t)pid * P * dvp;
@@ -584,19 +602,21 @@ __global__ void k_export(sphkv_store_t st, const int64_t* __restrict__ offsets, 
   const int64_t abytes = ((int64_t)n * (d - 1) * b + 7) / 8;
   const int64_t rbytes = ((int64_t)n * rb + 7) / 8;
   auto bit_at = [&](uint64_t bit) { return (words[bit >> 5] >> (bit & 31)) & 1u; };
+  const int W = item_words(d, b);
   for (int64_t k = threadIdx.x; k < abytes; k += blockDim.x) {
     uint32_t byte = 0;
     for (int bb = 0; bb < 8; ++bb) {
       int64_t pos = k * 8 + bb;
       if (pos >= (int64_t)n * (d - 1) * b) break;
-      int64_t ci = pos / b;
+      int64_t ci = pos / b;  // reference SoA order: code (j, i) at j * count + i
       int bit = (int)(pos % b);
       int64_t j = ci / n, i = ci % n;
-      byte |= bit_at(((uint64_t)j * P + i) * b + bit) << bb;
+      const int sb = (int)j * b + bit;  // bit of item i's string
+      byte |= ((words[wi_word((int)i, sb >> 5, W)] >> (sb & 31)) & 1u) << bb;
     }
     o[k] = (uint8_t)byte;
   }
-  const uint64_t rbase = (uint64_t)(d - 1) * P * b;
+  const uint64_t rbase = angle_part_bytes(d, P, b) * 8;
   for (int64_t k = threadIdx.x; k < rbytes; k += blockDim.x) {
     uint32_t byte = 0;
     for (int bb = 0; bb < 8; ++bb) {

@@ -44,8 +44,15 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint64_t* bar, uint32_t pari
   return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#ifdef SPHKV_WAIT_SLEEP
   while (!mbar_try_wait_sleep(bar, parity)) {
   }
+#else
+  // plain try_wait (hardware-bounded wait, no NANOSLEEP fallback): wakes as
+  // soon as the phase completes
+  while (!mbar_try_wait(bar, parity)) {
+  }
+#endif
 }
 
 // ---- TMA-engine bulk copies (1-D, no tensor map) -------------------------

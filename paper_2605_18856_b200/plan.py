@@ -60,10 +60,23 @@ def _page_bytes(rows, tiers, d, d_v, P):
     return PAGE_HEADER_BYTES + code + 2 * c * d_v, -(-c // ti)
 
 
-# Planner cost of one retained item beyond its stream bytes: the logit work of
-# an ADA item (127 LUT/FMA rows) takes about as long as streaming this many
-# bytes at the kernel's rate, so units are balanced on bytes + ITEM_COST*items.
-ITEM_COST = 160
+# Planner cost model.  k_ada_decode is bound by the on-chip work per item
+# (feature recurrence, LUT traffic), not by its bytes, and that work depends
+# on the tier's angle width: measured per-item cost on a B200 (tools/
+# tier_cost.py, profiles/r1*_tier_cost.log), in picoseconds per item at
+# d = 128, one layer of 8 KV heads x 128K items.  Units are balanced on
+# estimated time = items x cost(b_theta) (+ a small per-page term), so every
+# CTA of a one-unit-per-CTA plan finishes together.
+PS_PER_ITEM = {1: 90, 2: 90, 3: 95, 4: 95, 5: 117, 6: 117, 7: 135, 8: 150, 9: 160, 10: 165,
+               11: 170, 12: 177, 13: 400, 14: 430, 15: 470, 16: 500}
+PAGE_COST_PS = 200
+
+
+def _page_cost(rows, d):
+    ab = rows["abits"].astype(np.int64)
+    per = np.array([PS_PER_ITEM.get(int(b), 200) for b in range(17)], dtype=np.int64)[ab]
+    scale = max(d - 1, 1) / 127.0  # work scales with the d-1 code rows
+    return (rows["count"].astype(np.int64) * per * scale).astype(np.int64) + PAGE_COST_PS
 
 
 def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
@@ -80,7 +93,7 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
     if ranges is None:
         ranges = [(0, int(plen[g])) for g in groups]
     pbytes, ptiles = _page_bytes(rows, store.tiers, store.d, store.d_v, store.page_size)
-    pbytes = pbytes + ITEM_COST * rows["count"].astype(np.int64)
+    pbytes = _page_cost(rows, store.d)  # balance on estimated time, not bytes
     lists = [ptr[g, rb:re] for g, (rb, re) in zip(groups, ranges)]
     total = sum(int(pbytes[l].sum()) for l in lists)
     target = max(total // max(grid * units_per_cta, 1), 1)
@@ -131,8 +144,8 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
 
 
 def split_ranges(page_bytes, world):
-    """Split one pointer list (per-page stream bytes, pointer order) into
-    `world` contiguous ranges balanced by bytes, not page count (tiers differ
+    """Split one pointer list (per-page cost, pointer order) into
+    `world` contiguous ranges balanced by cost, not page count (tiers differ
     in bytes per item).  Range r ends at the first page whose cumulative bytes
     reach (r+1)/world of the total; ranges may be empty."""
     b = np.asarray(page_bytes, dtype=np.int64)
@@ -153,8 +166,8 @@ def split_ranges(page_bytes, world):
 def rank_ranges(store, groups, rank, world):
     """This rank's pointer-list range of every group (page-range split)."""
     n, rows, plen, ptr = store._host()
-    pbytes, _ = _page_bytes(rows, store.tiers, store.d, store.d_v, store.page_size)
-    return [split_ranges(pbytes[ptr[g, : plen[g]]], world)[rank] for g in groups]
+    cost = _page_cost(rows, store.d)  # ranks balanced on estimated time
+    return [split_ranges(cost[ptr[g, : plen[g]]], world)[rank] for g in groups]
 
 
 def plan_store_range(store, groups, rank, world, grid=SM_COUNT, units_per_cta=2,

@@ -123,8 +123,12 @@ def _page_formulas(count, capacity, tier: TierSpec, d, d_v):
 
 
 def code_block_bytes(d, P, abits, rbits):
-    bits = (d - 1) * P * abits + P * rbits
-    return ((bits + 7) // 8 + 15) // 16 * 16
+    """Device code block of one page (word-interleaved angle part + radius
+    row, see include/sphkv_b200.h); mirrors common.cuh:code_block_bytes."""
+    words = (((d - 1) * abits + 31) // 32 + 3) // 4 * 4
+    angle = (P + 31) // 32 * words * 128
+    rbytes = (P * rbits + 7) // 8
+    return angle + (rbytes + 15) // 16 * 16
 
 
 class PageView:

@@ -135,14 +135,30 @@ def test_pack_pages_bit_exact(sk, golden, name):
     g = golden("store")
     st, *_ = pack_case(sk, g, name)
     check_store_bytes(st, g, name + "_pack_")
-    # full pages: the device code block IS the reference stream (stride = P)
-    P = st.page_size
+    # the device block (word-interleaved item-major layout, sphkv_b200.h)
+    # holds exactly the reference codes: decode it on the host and compare
+    # with the reference SoA stream (store.py:205-208)
+    P, d = st.page_size, st.d
     for p in st.pages:
-        if p.count == P:
-            row = st._host()[1][p.index]
-            nbytes = len(p.angle_stream())
-            dev = st.t_codes[int(row["code_off"]): int(row["code_off"]) + nbytes].cpu().numpy()
-            assert np.array_equal(dev, p.angle_stream())
+        if p.count == 0:
+            continue
+        row = st._host()[1][p.index]
+        b = int(row["abits"])
+        W = (((d - 1) * b + 31) // 32 + 3) // 4 * 4
+        nw = (P + 31) // 32 * W * 32
+        off = int(row["code_off"])
+        words = st.t_codes[off: off + 4 * nw].cpu().numpy().view(np.uint32)
+        i = np.arange(p.count)[:, None]
+        w = np.arange(W)[None, :]
+        idx = (((i >> 5) * (W >> 2) + (w >> 2)) * 32 + (i & 31)) * 4 + (w & 3)
+        strings = words[idx].astype(np.uint64)  # [count, W]
+        bits = ((strings[:, :, None] >> np.arange(32, dtype=np.uint64)) & 1).reshape(p.count, -1)
+        j = np.arange(d - 1)
+        codes = np.zeros((p.count, d - 1), dtype=np.uint64)
+        for t in range(b):
+            codes |= bits[:, j * b + t] << np.uint64(t)
+        want = O.unpack_bits(p.angle_stream(), b, p.count * (d - 1)).reshape(d - 1, p.count).T
+        assert np.array_equal(codes, want.astype(np.uint64))
 
 
 @pytest.mark.parametrize("name", CASES)
