@@ -403,8 +403,20 @@ __device__ __forceinline__ void fused_kernel_exit(const FusedCtl& f) {
 // ---------------------------------------------------------------------------
 // ADA kernel
 // ---------------------------------------------------------------------------
+#ifdef SPHKV_DBG_TIMING  // per-CTA start/end (globaltimer ns) of the last launch
+__device__ unsigned long long g_cta_t[2 * 1024];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 template <int GP>
 __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p) {
+#ifdef SPHKV_DBG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x] = gtimer();
+#endif
   extern __shared__ __align__(1024) uint8_t smem[];
   const sphkv_store_t& st = p.st;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -447,18 +459,70 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
     }
   }
   if (p.lut_global == nullptr) lut_fill(smem, st.tiers, st.n_tiers, p.lut_off, threadIdx.x, blockDim.x);
-  ptx::griddep_wait();  // inputs below (q, plan, store tables) may come from the previous grid
-  __syncthreads();
-  ptx::griddep_launch_dependents();
-  bool lut_ready = false;
-
-  const float qscale = kLog2e * rsqrtf((float)d);
+  // L2 prefetch, PF_DIST tiles ahead of the claim order: the tile's code
+  // granules (contiguous in the WI layout), its radius row with the
+  // page's first tile, and (SPHKV_PF_V) its fp16 V block, so the V bulk
+  // copy and the code loads hit L2 and many more bytes are in flight per
+  // SM than the smem rings alone could hold.
+  auto prefetch_tile = [&](int t, int nt) {
+    if (t < nt && lane == 0) {
+      const TileEntry tn = tiles[t];
+      const int sb = tn.sub_off >> 24;
+      const sphkv_page_t pn = st.pages[tn.page];
+      const uint64_t W4 = (uint64_t)item_words(d, pn.abits) * 128;  // bytes per granule
+      const int g0 = sb * TI / 32, ng = (TI + 31) / 32;
+      ptx::bulk_prefetch_l2(st.codes + pn.code_off + g0 * W4, (uint32_t)(ng * W4));
+      if (sb == 0) {
+        const uint64_t ab = angle_part_bytes(d, P, pn.abits);
+        ptx::bulk_prefetch_l2(st.codes + pn.code_off + ab,
+                              (uint32_t)(code_block_bytes(d, P, pn.abits, pn.rbits) - ab));
+      }
+#if SPHKV_PF_V
+      ptx::bulk_prefetch_l2(st.values + ((size_t)tn.page * P + (size_t)sb * TI) * dvp, vbytes);
+#endif
+    }
+  };
+  // Also independent of the previous grid (it only reads q and writes
+  // outputs): the first unit's tile list and its first L2 prefetches.
   __shared__ int s_flag, s_next;
   __shared__ float s_ml[16];
+  int u = fused_first_unit(p.fz, &s_next);
+  if (u < p.n_units && warp == 0) {
+    build_tiles(st, p.units[u], TI, tiles, ntiles_s, lane);
+    if (lane == 0) *tile_ctr = 0;
+  }
+  __syncthreads();
+  // V tile producer (lane 0 of the first PV warp): bulk copy of tile k's fp16
+  // V block into ring slot (gbase + k) % NV once every PV warp released it
+  const uint64_t vpol = ptx::policy_evict_first();
+  auto issue_v = [&](int k, uint32_t gb) {
+    const uint32_t gk = gb + k;
+    const int vs = gk % ADA_NV;
+    ptx::mbar_wait(&v_empty[vs], ((gk / ADA_NV) & 1) ^ 1);
+    const TileEntry te = tiles[k];
+    const int sub = te.sub_off >> 24;
+    const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)sub * TI) * dvp;
+    ptx::fence_proxy_async();  // order earlier ldmatrix reads of the slot
+    ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
+    ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
+  };
+  if (u < p.n_units && warp < ADA_NL)
+    for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, *ntiles_s);
+  if (u < p.n_units && warp == ADA_NL && lane == 0)
+    for (int k = 0; k < *ntiles_s && k < ADA_NV; ++k) issue_v(k, 0u);
+  ptx::griddep_wait();  // inputs below (q) may come from the previous grid
+#ifdef SPHKV_DBG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x] = gtimer();
+#endif
+  __syncthreads();
+  ptx::griddep_launch_dependents();
+  bool lut_ready = false, first = true;
+
+  const float qscale = kLog2e * rsqrtf((float)d);
   uint32_t gbase = 0;  // running tile sequence number (barrier phases)
-  for (int u = fused_first_unit(p.fz, &s_next); u < p.n_units;) {
+  for (; u < p.n_units; first = false) {
     const sphkv_unit_t unit = p.units[u];
-    if (warp == 0) {
+    if (!first && warp == 0) {
       build_tiles(st, unit, TI, tiles, ntiles_s, lane);
       if (lane == 0) *tile_ctr = 0;
     }
@@ -481,37 +545,15 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       }
       // tiles are claimed dynamically (smem counter) to balance the warps;
       // the P slot of tile k is k % NS whoever computes it.
-      // L2 prefetch, PF_DIST tiles ahead of the claim order: the tile's code
-      // granules (contiguous in the WI layout), its radius row with the
-      // page's first tile, and (SPHKV_PF_V) its fp16 V block, so the V bulk
-      // copy and the code loads hit L2 and many more bytes are in flight per
-      // SM than the smem rings alone could hold.
-      auto prefetch_tile = [&](int t) {
-        if (t < nt && lane == 0) {
-          const TileEntry tn = tiles[t];
-          const int sb = tn.sub_off >> 24;
-          const sphkv_page_t pn = st.pages[tn.page];
-          const uint64_t W4 = (uint64_t)item_words(d, pn.abits) * 128;  // bytes per granule
-          const int g0 = sb * TI / 32, ng = (TI + 31) / 32;
-          ptx::bulk_prefetch_l2(st.codes + pn.code_off + g0 * W4, (uint32_t)(ng * W4));
-          if (sb == 0) {
-            const uint64_t ab = angle_part_bytes(d, P, pn.abits);
-            ptx::bulk_prefetch_l2(st.codes + pn.code_off + ab,
-                                  (uint32_t)(code_block_bytes(d, P, pn.abits, pn.rbits) - ab));
-          }
-#if SPHKV_PF_V
-          ptx::bulk_prefetch_l2(st.values + ((size_t)tn.page * P + (size_t)sb * TI) * dvp, vbytes);
-#endif
-        }
-      };
 #pragma unroll 1
-      for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t);
+      if (!first)
+        for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, nt);
       for (;;) {
         int k = 0;
         if (lane == 0) k = atomicAdd(tile_ctr, 1);
         k = __shfl_sync(0xffffffffu, k, 0);
         if (k >= nt) break;
-        prefetch_tile(k + SPHKV_PF_DIST);
+        prefetch_tile(k + SPHKV_PF_DIST, nt);
         const uint32_t gk = gbase + k;
         const TileEntry te = tiles[k];
         const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
@@ -556,20 +598,8 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       const int mtw = (MT + ADA_NPV - 1) / ADA_NPV;
       const int mt0 = pw * mtw;
       const int mtn = max(0, min(mtw, MT - mt0));
-      const uint64_t vpol = ptx::policy_evict_first();
-      auto issue_v = [&](int k) {
-        const uint32_t gk = gbase + k;
-        const int vs = gk % ADA_NV;
-        ptx::mbar_wait(&v_empty[vs], ((gk / ADA_NV) & 1) ^ 1);
-        const TileEntry te = tiles[k];
-        const int sub = te.sub_off >> 24;
-        const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)sub * TI) * dvp;
-        ptx::fence_proxy_async();  // order earlier ldmatrix reads of the slot
-        ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
-        ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
-      };
-      if (pw == 0 && lane == 0)
-        for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k);
+      if (!first && pw == 0 && lane == 0)
+        for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k, gbase);
       PVState<ADA_MTW> s;
       pv_init(s);
       const bool fast_pv = (dvp == 128 && TI == 128 && mtn == ADA_MTW);
@@ -590,7 +620,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         if (lane == 0) {
           ptx::mbar_arrive(&p_empty[ps]);
           ptx::mbar_arrive(&v_empty[vs]);
-          if (pw == 0 && k + ADA_NV < nt) issue_v(k + ADA_NV);
+          if (pw == 0 && k + ADA_NV < nt) issue_v(k + ADA_NV, gbase);
         }
       }
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
@@ -603,6 +633,9 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
     u = p.fz.dynamic ? s_next : u + gridDim.x;
   }
   fused_kernel_exit(p.fz);
+#ifdef SPHKV_DBG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x + 1] = gtimer();
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1077,6 +1110,19 @@ extern "C" int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const flo
   int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
   if (rc) return rc;
   return dense_decode_impl(st, q, G, units, n_units, partials, grid, f, stream);
+}
+
+// Debug builds (-DSPHKV_DBG_TIMING) only: per-CTA (start, end) globaltimer of
+// the last ADA launch, 2 * n values; not declared in the public header.
+extern "C" int sphkv_debug_cta_times(unsigned long long* out_host, int n) {
+#ifdef SPHKV_DBG_TIMING
+  SPHKV_CUDA_TRY(cudaMemcpyFromSymbol(out_host, g_cta_t, sizeof(unsigned long long) * 2 * n));
+  return SPHKV_OK;
+#else
+  (void)out_host;
+  (void)n;
+  return fail(SPHKV_E_UNSUPPORTED, "built without SPHKV_DBG_TIMING");
+#endif
 }
 
 extern "C" int sphkv_lse_merge_ex(const float* partials, const int32_t* slot_begin,
