@@ -47,6 +47,19 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def load_traffic(cfg_name, kernel="k_ada_decode"):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum
+    of one `ncu --set full` launch of this config), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t[cfg_name][kernel]
+        return int(e["dram_bytes_per_launch"]), e["source"]
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -80,7 +93,7 @@ class ClockSampler:
                     self.samples.append([x.strip() for x in out[0].split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def stop(self):
         self._stop.set()
@@ -256,7 +269,7 @@ def cpu_oracle_sample(W, rank, steps=3, budget_s=20.0):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
@@ -466,6 +479,7 @@ def main():
         bytes_total = bytes_total // world
     alg_bytes_per_launch = (bytes_total + qbytes + part_bytes) / n_launch
     peak, peak_kind = load_peaks()
+    traffic, traffic_src = load_traffic(args.config) if world == 1 else (None, None)
     achieved = alg_bytes_per_launch / (dec_ms * 1e-3) / 1e9
     kv_bytes_token = W["info"]["resident_ada"] / T
 
@@ -531,7 +545,8 @@ def main():
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32 (fp16 V, angle codes)", "data": "synthetic", "config": config,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None,
+                             "frac": achieved / peak, "traffic": traffic,
+                             "traffic_source": traffic_src,
                              "kernel": "k_ada_decode", "kernel_ms_per_launch": dec_ms,
                              "alg_bytes_per_launch": int(alg_bytes_per_launch),
                              "peak_kind": peak_kind},

@@ -248,6 +248,12 @@ def test_split_merge_equals_single_pass(sk):
     one = sk.ada_decode(st, wl.queries, sk.plan_store(st, grid=2, units_per_cta=1))
     many = sk.ada_decode(st, wl.queries, sk.plan_store(st, grid=148, units_per_cta=4))
     assert torch.allclose(one, many, rtol=2e-5, atol=2e-5)
+    # repeated fused launches reuse the self re-arming split counters
+    plan = sk.plan_store(st, grid=148, units_per_cta=1)
+    for _ in range(3):
+        again = sk.ada_decode(st, wl.queries, plan)
+        assert torch.allclose(one, again, rtol=2e-5, atol=2e-5)
+    assert int(plan.ctl.abs().sum()) == 0
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
@@ -435,3 +441,18 @@ def test_scalar_append_scoring_matches_golden(sk, golden):
             got = sk.score_and_best_tier(sk.StateId(int(l), int(h), int(i)), key, feat, tiers,
                                          float(lam), protected=bool(g[p + "prot"][l, h, i]))
             assert got[0] == int(tid) and got[1] == s and got[2] == nu
+
+
+@pytest.mark.parametrize("name", ["small", "rows"])
+def test_compute_features_matches_reference_golden(sk, golden, name):
+    """controller.compute_features (controller.py:99-142) on the device (fp64)
+    vs the reference's own outputs on the same workload."""
+    from types import SimpleNamespace
+
+    g = golden("features")
+    p = name + "_"
+    wl = SimpleNamespace(keys=g[p + "keys"], queries=g[p + "queries"], segments=g[p + "segments"])
+    feat = sk.compute_features(wl, sk.ControllerConfig())
+    np.testing.assert_allclose(feat.u_hat, g[p + "u_hat"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(feat.s_hat, g[p + "s_hat"], rtol=1e-9, atol=1e-12)
+    assert abs(feat.r_q - float(g[p + "r_q"])) <= 1e-12 * abs(float(g[p + "r_q"]))
