@@ -17,28 +17,36 @@ namespace sphkv {
 
 constexpr int LUT_MAX_BITS = 12;
 #ifndef SPHKV_LUT_KB
-#define SPHKV_LUT_KB 90
+#define SPHKV_LUT_KB 110
 #endif
 constexpr int LUT_BUDGET_BYTES = SPHKV_LUT_KB * 1024;
 
 // Polar (cos, sin) tables in shared memory, one per tier with B <= 12.
-//  * B <= 4: "row-pair" tables indexed by the codes of two consecutive rows
-//    (j, j+1) of the same item (2B contiguous bits of its code string); an
-//    entry (cos a_j, sin a_j cos a_j+1, sin a_j sin a_j+1, 0) -- products
-//    taken in fp64, rounded once -- is one LDS.128 that advances the feature
-//    recurrence by two rows.
+//  * B <= 2: "quad-row" tables indexed by the codes of four consecutive rows
+//    (j..j+3) of one item (4B contiguous bits of its code string): part A,
+//    16-byte entries (c0, s0 c1, s0 s1 c2, s0 s1 s2 c3), replicated 8x, and
+//    part B, 4-byte entries s0 s1 s2 s3 (the running sine product's factor),
+//    replicated 16x; products taken in fp64 and rounded once.  One LDS.128 +
+//    one LDS.32 advance the feature recurrence by four rows.  Looking part A
+//    up with the top two codes zero gives (c0, s0 c1, s0 s1, 0) -- a row pair.
+//  * 3 <= B <= 4: "row-pair" tables: entry (c_j, s_j c_j+1, s_j s_j+1, 0),
+//    one LDS.128 per two rows.
 //  * 5 <= B <= 12: single-code tables, entry (cos, sin) = one LDS.64.
-// Random gathers from a small table bank-conflict heavily, so when the budget
-// allows a table is stored REP times interleaved: entry e of copy r lives at
-// (e * REP + r) * entry_bytes and lane L reads copy L % REP.  REP = 8 for
-// 16-byte entries (8 lanes per LDS.128 phase) and 16 for 8-byte entries
-// (16 lanes per LDS.64 phase), so every phase hits distinct banks and the
-// entry stride is 128 bytes either way.
-__host__ __device__ constexpr int lut_group(int B) { return B <= 4 ? 2 : 1; }
-__host__ __device__ constexpr int lut_entry_bytes(int B) { return 8 * lut_group(B); }
-__host__ __device__ constexpr int lut_rep(int B) { return lut_group(B) == 2 ? 8 : 16; }
+// Random gathers from a small table bank-conflict heavily, so a table may be
+// stored REP times interleaved: entry e of copy r lives at (e * REP + r) *
+// entry_bytes and lane L reads copy L % REP.  REP = 8 for 16-byte entries (8
+// lanes per LDS.128 phase), 16 for 8-byte entries (16 lanes per LDS.64
+// phase), so every phase hits distinct banks and the entry stride is 128
+// bytes either way.  Quad tables are always replicated (the 2-bit tier holds
+// most items); the others as the budget allows, narrow tiers first.
+__host__ __device__ constexpr int lut_group(int B) { return B <= 2 ? 4 : (B <= 4 ? 2 : 1); }
+__host__ __device__ constexpr int lut_entry_bytes(int B) { return lut_group(B) == 1 ? 8 : 16; }
+__host__ __device__ constexpr int lut_rep(int B) { return lut_group(B) == 1 ? 16 : 8; }
+__host__ __device__ constexpr int lut_quad_b_rep() { return 16; }
 __host__ __device__ constexpr int lut_bytes(int B, bool repl) {
-  return (1 << (lut_group(B) * B)) * lut_entry_bytes(B) * (repl ? lut_rep(B) : 1);
+  return lut_group(B) == 4
+             ? (1 << (4 * B)) * (16 * 8 + 4 * lut_quad_b_rep())  // parts A + B, replicated
+             : (1 << (lut_group(B) * B)) * lut_entry_bytes(B) * (repl ? lut_rep(B) : 1);
 }
 
 // Encoded per-tier table descriptor: (byte offset << 1) | replicated, or -1.
@@ -46,18 +54,20 @@ __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n
                                                 int off[SPHKV_MAX_TIERS]) {
   for (int t = 0; t < SPHKV_MAX_TIERS; ++t) off[t] = -1;
   int minimal = 0;
+  bool repl[SPHKV_MAX_TIERS] = {};
   for (int t = 1; t < n_tiers; ++t) {
     const int b = tiers[t].angle_bits;
-    if (b <= LUT_MAX_BITS && minimal + lut_bytes(b, false) <= LUT_BUDGET_BYTES) {
-      minimal += lut_bytes(b, false);
+    const bool quad = lut_group(b) == 4;
+    if (b <= LUT_MAX_BITS && minimal + lut_bytes(b, quad) <= LUT_BUDGET_BYTES) {
+      minimal += lut_bytes(b, quad);
       off[t] = 0;  // has a table; placed below
+      repl[t] = quad;
     }
   }
-  bool repl[SPHKV_MAX_TIERS] = {};
   int total = minimal;
   for (int pass_b = 1; pass_b <= LUT_MAX_BITS; ++pass_b)  // narrow tiers first
     for (int t = 1; t < n_tiers; ++t)
-      if (off[t] == 0 && tiers[t].angle_bits == pass_b) {
+      if (off[t] == 0 && !repl[t] && tiers[t].angle_bits == pass_b) {
         const int extra = lut_bytes(pass_b, true) - lut_bytes(pass_b, false);
         if (total + extra <= LUT_BUDGET_BYTES) {
           repl[t] = true;
@@ -73,9 +83,27 @@ __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n
   return used;
 }
 
-// Fill one (entry, copy) of a table: tier bits B, entry e, copy r.
+// Fill one (entry, copy) of a table: tier bits B, entry e, copy r.  Quad
+// tables: copies r < 8 are part A, 8 <= r < 24 part B (copy r - 8).
 __device__ inline void lut_write_entry(uint8_t* dst, int B, bool repl, int e, int r) {
   const double step = kPi / (double)((1u << B) - 1u);
+  if (lut_group(B) == 4) {
+    const uint32_t M = (1u << B) - 1u;
+    double sn[4], cs[4];
+    for (int k = 0; k < 4; ++k) sincos((double)((e >> (k * B)) & M) * step, &sn[k], &cs[k]);
+    const int nA = (1 << (4 * B)) * 128;
+    if (r < 8) {
+      float* out = reinterpret_cast<float*>(dst + ((size_t)e * 8 + r) * 16);
+      out[0] = (float)cs[0];
+      out[1] = (float)(sn[0] * cs[1]);
+      out[2] = (float)(sn[0] * sn[1] * cs[2]);
+      out[3] = (float)(sn[0] * sn[1] * sn[2] * cs[3]);
+    } else {
+      float* out = reinterpret_cast<float*>(dst + nA + ((size_t)e * lut_quad_b_rep() + (r - 8)) * 4);
+      out[0] = (float)(sn[0] * sn[1] * sn[2] * sn[3]);
+    }
+    return;
+  }
   const int R = repl ? lut_rep(B) : 1;
   float* out = reinterpret_cast<float*>(dst + ((size_t)e * R + r) * lut_entry_bytes(B));
   if (lut_group(B) == 1) {
@@ -102,7 +130,7 @@ __device__ inline void lut_fill(uint8_t* lut, const sphkv_tier_t* tiers, int n_t
     if (enc[t] < 0) continue;
     const int B = tiers[t].angle_bits;
     const bool repl = enc[t] & 1;
-    const int R = repl ? lut_rep(B) : 1;
+    const int R = lut_group(B) == 4 ? 8 + lut_quad_b_rep() : (repl ? lut_rep(B) : 1);
     const int n = (1 << (lut_group(B) * B)) * R;
     for (int i = tid; i < n; i += nthreads)
       lut_write_entry(lut + (enc[t] >> 1), B, repl, i / R, i % R);
@@ -208,10 +236,60 @@ template <int B, int GP, int MODE, int STR, int RR = Period<B>::R>
 __device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::WP],
                                             const uint8_t* sm, uint32_t qrow0, uint32_t tb,
                                             uint32_t orv, float (&prod)[4],
-                                            ptx::f2 (&acc)[4][GP]) {
+                                            ptx::f2 (&acc)[4][GP], uint32_t qb_off = 0) {
   constexpr int R = Period<B>::R, WP = Period<B>::WP;
   constexpr uint32_t QR = GP * 8;
-  if constexpr (MODE == 2) {
+  if constexpr (MODE == 4) {
+    // quad-row table: part A at tb, part B at tb + qb_off (4-byte entries, 16
+    // copies, 64-byte stride); a trailing row pair uses part A alone
+    static_assert(RR % 2 == 0, "row pairs");
+    constexpr int NQ = RR / 4;
+    const uint32_t orv_b = (uint32_t)(threadIdx.x & 15) * 4u;
+    static_for<NQ>([&](auto pc) {
+      constexpr int p = decltype(pc)::value;
+      ptx::f2 q0[GP], q1[GP], q2[GP], q3[GP];
+      load_q<GP>(sm, qrow0 + (4 * p) * QR, q0);
+      load_q<GP>(sm, qrow0 + (4 * p + 1) * QR, q1);
+      load_q<GP>(sm, qrow0 + (4 * p + 2) * QR, q2);
+      load_q<GP>(sm, qrow0 + (4 * p + 3) * QR, q3);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t aa = field_addr<4 * B, 4 * p * B, 7, WP>(cw[k], orv);
+        const uint32_t ab = field_addr<4 * B, 4 * p * B, 6, WP>(cw[k], orv_b);
+        const float4 e = *reinterpret_cast<const float4*>(sm + tb + aa);
+        const float sp = *reinterpret_cast<const float*>(sm + tb + qb_off + ab);
+        const ptx::f2 pp = ptx::f2_make(prod[k], prod[k]);
+        const ptx::f2 f01 = ptx::f2_mul(pp, ptx::f2_make(e.x, e.y));
+        const ptx::f2 f23 = ptx::f2_mul(pp, ptx::f2_make(e.z, e.w));
+        prod[k] *= sp;
+#pragma unroll
+        for (int g = 0; g < GP; ++g) {
+          ptx::f2_fma_s_acc(ptx::f2_lo(f01), q0[g], acc[k][g]);
+          ptx::f2_fma_s_acc(ptx::f2_hi(f01), q1[g], acc[k][g]);
+          ptx::f2_fma_s_acc(ptx::f2_lo(f23), q2[g], acc[k][g]);
+          ptx::f2_fma_s_acc(ptx::f2_hi(f23), q3[g], acc[k][g]);
+        }
+      }
+    });
+    if constexpr (RR % 4 == 2) {  // trailing pair: top two codes of the index zero
+      constexpr int j0 = 4 * NQ;
+      ptx::f2 qa[GP], qb[GP];
+      load_q<GP>(sm, qrow0 + j0 * QR, qa);
+      load_q<GP>(sm, qrow0 + (j0 + 1) * QR, qb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t a = field_addr<2 * B, j0 * B, 7, WP>(cw[k], orv);
+        const float4 e = *reinterpret_cast<const float4*>(sm + tb + a);
+        const ptx::f2 f = ptx::f2_mul(ptx::f2_make(prod[k], prod[k]), ptx::f2_make(e.x, e.y));
+        prod[k] *= e.z;
+#pragma unroll
+        for (int g = 0; g < GP; ++g) {
+          ptx::f2_fma_s_acc(ptx::f2_lo(f), qa[g], acc[k][g]);
+          ptx::f2_fma_s_acc(ptx::f2_hi(f), qb[g], acc[k][g]);
+        }
+      }
+    }
+  } else if constexpr (MODE == 2) {
     static_assert(RR % 2 == 0, "row pairs");
     static_for<RR / 2>([&](auto pc) {
       constexpr int p = decltype(pc)::value;
@@ -275,8 +353,9 @@ __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int s
   constexpr int R = Period<B>::R, WP = Period<B>::WP;
   constexpr int NP = D - 2;      // polar rows
   constexpr int NFULL = NP / R;  // whole periods of polar rows
-  constexpr int EB = (MODE == 2) ? 16 : 8;
+  constexpr int EB = (MODE == 2 || MODE == 4) ? 16 : 8;
   constexpr int STR = REPL ? 7 : ((MODE == 2) ? 4 : 3);
+  const uint32_t qb_off = (MODE == 4) ? (uint32_t)((1 << (4 * B)) * 128) : 0u;
   constexpr uint32_t QR = GP * 8;
   const uint32_t orv = REPL ? (uint32_t)(lane % (128 / EB)) * EB : 0u;
   const uint32_t* blk = reinterpret_cast<const uint32_t*>(blkb);
@@ -301,7 +380,7 @@ __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int s
     for (int k = 0; k < 4; ++k)
 #pragma unroll
       for (int i = 0; i < WP; ++i) nw[k][i] = item_word<W>(blk, sub, k, lane, min(wn + i, W - 1));
-    period_rows<B, GP, MODE, STR>(cw, sm, qs + per * R * QR, tb, orv, prod, acc);
+    period_rows<B, GP, MODE, STR>(cw, sm, qs + per * R * QR, tb, orv, prod, acc, qb_off);
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -311,7 +390,7 @@ __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int s
   // NP = D-2, whose code lies in the same period window
   constexpr int RR = NP - NFULL * R;
   if constexpr (RR > 0)
-    period_rows<B, GP, MODE, STR, RR>(cw, sm, qs + NFULL * R * QR, tb, orv, prod, acc);
+    period_rows<B, GP, MODE, STR, RR>(cw, sm, qs + NFULL * R * QR, tb, orv, prod, acc, qb_off);
   {
     ptx::f2 qa[GP], qb[GP];
     load_q<GP>(sm, qs + NP * QR, qa);
@@ -441,18 +520,20 @@ __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, 
   if (P % 128 != 0) {
     // pages narrower than a tile: generic path (guards items >= P)
   } else if (d == 128) {
-    if (B == 2 && has && repl) { SPHKV_WI(2, 128, 2, true); return; }
+    if (B == 2 && has) { SPHKV_WI(2, 128, 4, true); return; }
     if (B == 4 && has && repl) { SPHKV_WI(4, 128, 2, true); return; }
     if (B == 4 && has && !repl) { SPHKV_WI(4, 128, 2, false); return; }
     if (B == 6 && has && repl) { SPHKV_WI(6, 128, 1, true); return; }
+    if (B == 6 && has && !repl) { SPHKV_WI(6, 128, 1, false); return; }
     if (B == 7 && has && repl) { SPHKV_WI(7, 128, 1, true); return; }
+    if (B == 7 && has && !repl) { SPHKV_WI(7, 128, 1, false); return; }
 #ifdef SPHKV_MUFU12
     if (B == 12) { SPHKV_WI(12, 128, 3, false); return; }
 #endif
     if (B == 12 && has && !repl) { SPHKV_WI(12, 128, 1, false); return; }
     if (B == 15 && !has) { SPHKV_WI(15, 128, 0, false); return; }
   } else if (d == 64) {
-    if (B == 2 && has && repl) { SPHKV_WI(2, 64, 2, true); return; }
+    if (B == 2 && has) { SPHKV_WI(2, 64, 4, true); return; }
     if (B == 4 && has && repl) { SPHKV_WI(4, 64, 2, true); return; }
     if (B == 6 && has && repl) { SPHKV_WI(6, 64, 1, true); return; }
     if (B == 7 && has && repl) { SPHKV_WI(7, 64, 1, true); return; }

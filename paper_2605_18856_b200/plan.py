@@ -68,10 +68,11 @@ def _page_bytes(rows, tiers, d, d_v, P):
 # estimated time = items x cost(b_theta) (+ a small per-page term), so every
 # CTA of a one-unit-per-CTA plan finishes together.
 # (refined by a least-squares fit of per-CTA durations of mixed-tier c5
-# launches, tools/cta_times.py: 11.3 / 12.5 / 16.6 / 24.5 ns per item per CTA
-# for b_theta = 2 / 4 / 7 / 12 -- same ratios, scaled to the single-tier runs)
-PS_PER_ITEM = {1: 90, 2: 90, 3: 95, 4: 100, 5: 125, 6: 140, 7: 132, 8: 150, 9: 160, 10: 170,
-               11: 185, 12: 195, 13: 400, 14: 430, 15: 470, 16: 500}
+# launches, tools/cta_times.py: 9.95 / 14.4 / 17.6 / 24.2 ns per item per CTA
+# for b_theta = 2 / 4 / 7 / 12 with the quad-row 2-bit tables -- same ratios,
+# scaled to the single-tier runs)
+PS_PER_ITEM = {1: 80, 2: 80, 3: 120, 4: 116, 5: 140, 6: 190, 7: 141, 8: 160, 9: 170, 10: 180,
+               11: 190, 12: 195, 13: 400, 14: 430, 15: 470, 16: 500}
 PAGE_COST_PS = 200
 
 

@@ -43,6 +43,8 @@ for l in (0, 5):
     X = ab[:, [2, 4, 6, 7, 12]]
     coef, *_ = np.linalg.lstsq(X, dur[: len(pc)], rcond=None)
     print("   fitted us/item by bits 2,4,6,7,12:", np.round(coef * 1e3, 2), "(ns)")
+    print("   dur by blockIdx%8:", [round(float(dur[np.arange(len(dur)) % 8 == r].mean()), 1) for r in range(8)])
+    print("   dur by blockIdx<74:", round(float(dur[:74].mean()), 1), round(float(dur[74:].mean()), 1))
     for i in np.argsort(-dur)[:5]:
         print("   slow cta", i, "dur %.1f" % dur[i], "pred %.1f" % (pc[i] / 1e6), "items by bits",
               {b: int(ab[i][b]) for b in range(16) if ab[i][b]})
