@@ -279,8 +279,6 @@ def main():
     ap.add_argument("--units-per-cta", type=int, default=1)
     ap.add_argument("--unfused", action="store_true",
                     help="separate LSE-merge launch per layer (default: merge fused in the decode)")
-    ap.add_argument("--static", action="store_true",
-                    help="static one-range-per-CTA split instead of the shared-cursor plan")
     ap.add_argument("--dynamic", action="store_true",
                     help="CTAs claim units from a global queue (longest first)")
     ap.add_argument("--fuse-layers", action="store_true",
@@ -345,8 +343,6 @@ def main():
 
     def ada_plan(s, groups):
         if world == 1:
-            if not (args.static or args.dynamic or args.unfused or args.units_per_cta != 1):
-                return planmod.plan_store_shared(s, groups=groups)
             return planmod.plan_store(s, groups=groups, units_per_cta=args.units_per_cta,
                                       dynamic=args.dynamic)
         return planmod.plan_store_range(s, groups, rank, world, units_per_cta=args.units_per_cta)
@@ -371,13 +367,6 @@ def main():
 
     def decode_layers(with_merge=True):
         for l, p in enumerate(plans):
-            if fused and p.shared:
-                _lib.check(lib.sphkv_ada_decode_shared(
-                    st.cptr, q.data_ptr(), G, p.units.data_ptr(), p.n_units, parts[l].data_ptr(),
-                    p.slot_group.data_ptr(), p.slot_begin.data_ptr(), len(p.group_ids),
-                    p.ctl.data_ptr(), outs[l].data_ptr(), p.tile_tab.data_ptr(),
-                    p.tab_begin.data_ptr(), p.cursors.data_ptr(), p.grid, sp))
-                continue
             if fused:
                 _lib.check(lib.sphkv_ada_decode_fused(
                     st.cptr, q.data_ptr(), G, p.units.data_ptr(), p.n_units, parts[l].data_ptr(),

@@ -262,20 +262,6 @@ int sphkv_ada_decode_fused(const sphkv_store_t* st, const float* q, int G,
                            int32_t* ctl, float* out, int dynamic, int grid,
                            cudaStream_t stream);
 
-/* ADA decode, shared-cursor mode: the n_g units (one per CTA, n_units <=
- * grid) of plan group g all cover the whole group and claim its tiles one at
- * a time from cursors[g], so the CTAs sharing a group finish together.
- * tile_tab int32 pairs (page, (sub << 24) | item offset within the group),
- * group g's tiles at [tab_begin[g], tab_begin[g+1]); cursors int32
- * [n_groups] and ctl [n_groups + 2] zero before the first call, left zero.
- * The split merge is fused as in sphkv_ada_decode_fused. */
-int sphkv_ada_decode_shared(const sphkv_store_t* st, const float* q, int G,
-                            const sphkv_unit_t* units, int n_units, float* partials,
-                            const int32_t* slot_group, const int32_t* slot_begin, int n_groups,
-                            int32_t* ctl, float* out, const int32_t* tile_tab,
-                            const int32_t* tab_begin, int32_t* cursors, int grid,
-                            cudaStream_t stream);
-
 /* Dense bf16 paged decode with the same unit/partial contract. */
 int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,
                        const sphkv_unit_t* units, int n_units, float* partials,

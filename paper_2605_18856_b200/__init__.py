@@ -17,7 +17,7 @@ from .controller import (ControllerConfig, ControllerFeatures, StateId, StateSco
                          score_states)
 from .decode import (AttentionOutput, ada_decode, angle_logits, dense_decode, dense_logits,
                      logit_drift_bound, lse_merge, softmax_mix, stable_softmax)
-from .plan import DecodePlan, plan_dense, plan_store, plan_store_shared
+from .plan import DecodePlan, plan_dense, plan_store
 from .store import (DenseStore, PagedStore, ResidentBreakdown, TrafficMeter, dense_mem_estimate,
                     pack_device, pack_pages_arrays)
 

@@ -97,8 +97,6 @@ def _declare(lib):
         "sphkv_lse_merge_ex": (c_int, [vp, vp, i, i64, i, i, i, vp, i, vp]),
         "sphkv_ada_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
         "sphkv_dense_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
-        "sphkv_ada_decode_shared": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, vp, vp, vp,
-                                            i, vp]),
         "sphkv_partial_floats": (c_int64, [i, i]),
     }
     for name, (res, args) in sig.items():

@@ -81,10 +81,6 @@ struct AdaParams {
   uint32_t smem_q, smem_tiles, smem_p, smem_v, smem_bar;  // byte offsets
   int pslot_bytes, prow_bytes, prows;  // P slot: prows rows of TI fp16 weights + header
   FusedCtl fz;
-  // shared-cursor mode: per plan group a tile table and a global claim cursor
-  const int2* tile_tab;      // (page, (sub << 24) | item offset in the group)
-  const int32_t* tab_begin;  // [n_groups + 1]
-  int32_t* cursors;          // [n_groups], caller-zeroed, left zeroed
 };
 
 __device__ __forceinline__ int tier_index(const sphkv_store_t& st, int tier_id) {
@@ -331,9 +327,6 @@ __device__ __forceinline__ void pv_write(const PVState<MTW>& s, float* part, int
 // zeroed): ctl[g] = finished splits of plan group g, ctl[n_groups] = unit
 // queue head, ctl[n_groups + 1] = CTAs done (the last one resets the queue).
 
-__device__ __noinline__ void merge_group_cta(const FusedCtl f, const float* partials, int gi,
-                                             int G, int d_v, float* s_ml);
-
 // Called by every thread after the unit's partial is written (all threads
 // have passed a __syncthreads since).  Returns through smem whether this CTA
 // merged; the caller's loop continues with *next_unit (dynamic mode).
@@ -355,13 +348,6 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
   }
   __syncthreads();
   if (!*s_flag) return;
-  merge_group_cta(f, partials, gi, G, d_v, s_ml);
-}
-
-// Merge all partial slots of plan group gi into its output rows, by the
-// whole CTA (called uniformly by every thread); re-arms the group's count.
-__device__ __noinline__ void merge_group_cta(const FusedCtl f, const float* partials, int gi,
-                                             int G, int d_v, float* s_ml) {
   __threadfence();
   const int b = f.slot_begin[gi], e = f.slot_begin[gi + 1];
   const int64_t stride = (int64_t)G * (d_v + 2);
@@ -388,7 +374,6 @@ __device__ __noinline__ void merge_group_cta(const FusedCtl f, const float* part
     const int g = i / d_v, j = i % d_v;
     const float M = s_ml[g], L = s_ml[8 + g];
     float a = 0.f;
-#pragma unroll 4
     for (int s = b; s < e; ++s) {
       const float m = __ldcg(partials + s * stride + g);
       if (m != -INFINITY) a += __ldcg(partials + s * stride + 2 * G + (int64_t)g * d_v + j) * exp2f(m - M);
@@ -651,285 +636,6 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 #ifdef SPHKV_DBG_TIMING
   if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x + 1] = gtimer();
 #endif
-}
-
-// ---------------------------------------------------------------------------
-// ADA kernel, shared-cursor mode
-// ---------------------------------------------------------------------------
-// The n_g CTAs assigned to one (seq, layer, kv-head) group share its tile
-// table and claim tiles one at a time from a global cursor, so they finish
-// together whatever their SM's speed (the static split left a ~20% tail); the
-// softmax state of a CTA covers any subset of the group's tiles (the LSE merge
-// is order-independent).  Each logit warp keeps its next claim in flight
-// while it computes the current tile; claimed tiles get a CTA-local sequence
-// number k in start order, which indexes the P ring, the V ring and the V
-// producer's lookup ring.
-constexpr int SH_RING = 32;
-
-// (explicit arguments, no lambda capturing the kernel parameters: taking the
-// address of the by-value AdaParams forces a local-memory copy of it)
-__device__ __forceinline__ void sh_prefetch(const int2* __restrict__ tab, int tab0, int ntab,
-                                            int gt, const sphkv_page_t* __restrict__ pages,
-                                            const uint8_t* codes, int d, int P, int TI) {
-  if ((threadIdx.x & 31) != 0 || gt >= ntab) return;
-  const int2 tn = tab[tab0 + gt];
-  const int sb = tn.y >> 24;
-  const sphkv_page_t pn = pages[tn.x];
-  const uint64_t W4 = (uint64_t)item_words(d, pn.abits) * 128;
-  const int g0 = sb * TI / 32, ng = (TI + 31) / 32;
-  ptx::bulk_prefetch_l2(codes + pn.code_off + g0 * W4, (uint32_t)(ng * W4));
-  if (sb == 0) {
-    const uint64_t ab = angle_part_bytes(d, P, pn.abits);
-    ptx::bulk_prefetch_l2(codes + pn.code_off + ab,
-                          (uint32_t)(code_block_bytes(d, P, pn.abits, pn.rbits) - ab));
-  }
-}
-
-// V copies of assigned sequence tiles [issued, upto), in order (lane 0)
-__device__ __forceinline__ void sh_issue_v(int& issued, int upto, const int2* ring,
-                                           const int* ring_seq, uint64_t* v_full,
-                                           uint64_t* v_empty, uint8_t* vslots, uint32_t vbytes,
-                                           const uint16_t* values, int P, int TI, int dvp,
-                                           uint64_t vpol) {
-  while (issued < upto) {
-    const volatile int* rs = ring_seq;
-    if (rs[issued % SH_RING] != issued) break;  // not assigned yet
-    const volatile int* rv = reinterpret_cast<const volatile int*>(ring + issued % SH_RING);
-    const int page = rv[0], sub = rv[1] >> 24;
-    const int vs = issued % ADA_NV;
-    ptx::mbar_wait(&v_empty[vs], ((issued / ADA_NV) & 1) ^ 1);
-    const uint16_t* src = values + ((size_t)page * P + (size_t)sub * TI) * dvp;
-    ptx::fence_proxy_async();
-    ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
-    ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
-    ++issued;
-  }
-}
-
-template <int GP>
-__global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_shared(const AdaParams p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  const sphkv_store_t& st = p.st;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int d = st.d, P = st.page_size, TI = p.TI, dvp = p.dvp, MT = dvp / 16;
-  const uint32_t vbytes = (uint32_t)TI * dvp * 2;
-  float2* qs = reinterpret_cast<float2*>(smem + p.smem_q);
-  int2* ring = reinterpret_cast<int2*>(smem + p.smem_tiles);       // [SH_RING] tile of seq k
-  int* ring_seq = reinterpret_cast<int*>(ring + SH_RING);            // [SH_RING] k stored
-  int* seq_ctr = ring_seq + SH_RING;                                 // tiles assigned
-  int* done_ctr = seq_ctr + 1;                                       // logit warps finished
-  uint8_t* pslots = smem + p.smem_p;
-  uint8_t* vslots = smem + p.smem_v;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
-  uint64_t* p_full = bars;
-  uint64_t* p_empty = bars + ADA_NS;
-  uint64_t* v_full = bars + 2 * ADA_NS;
-  uint64_t* v_empty = bars + 2 * ADA_NS + ADA_NV;
-  uint64_t* lut_bar = bars + 2 * ADA_NS + 2 * ADA_NV;
-  __shared__ float s_ml[16];
-  __shared__ int s_last;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < ADA_NS; ++i) {
-      ptx::mbar_init(&p_full[i], 1);
-      ptx::mbar_init(&p_empty[i], 1);
-    }
-    for (int i = 0; i < ADA_NV; ++i) {
-      ptx::mbar_init(&v_full[i], 1);
-      ptx::mbar_init(&v_empty[i], 1);
-    }
-    ptx::mbar_init(lut_bar, 1);
-    ptx::fence_mbar_init();
-    if (p.lut_global != nullptr && p.lut_bytes > 0) {
-      ptx::mbar_arrive_expect_tx(lut_bar, (uint32_t)p.lut_bytes);
-      ptx::bulk_g2s(smem, p.lut_global, (uint32_t)p.lut_bytes, lut_bar);
-    } else {
-      ptx::mbar_arrive(lut_bar);
-    }
-    *seq_ctr = 0;
-    *done_ctr = 0;
-  }
-  if (threadIdx.x < SH_RING) ring_seq[threadIdx.x] = -1;
-  if (p.lut_global == nullptr) lut_fill(smem, st.tiers, st.n_tiers, p.lut_off, threadIdx.x, blockDim.x);
-  ptx::griddep_wait();
-  __syncthreads();
-  ptx::griddep_launch_dependents();
-
-  const float qscale = kLog2e * rsqrtf((float)d);
-#pragma unroll 1
-  for (int u = blockIdx.x; u < p.n_units; u += gridDim.x) {  // one unit per CTA in practice
-    const sphkv_unit_t unit = p.units[u];
-    const int gi = p.fz.slot_group[unit.out_slot];
-    const int tab0 = p.tab_begin[gi], ntab = p.tab_begin[gi + 1] - tab0;
-    const int ncta = p.fz.slot_begin[gi + 1] - p.fz.slot_begin[gi];  // CTAs sharing the group
-    const float* qg = p.q + (size_t)unit.group * p.G * d;
-    for (int i = threadIdx.x; i < d * GP; i += blockDim.x) {
-      const int j = i / GP, g2 = i % GP;
-      const float a = (2 * g2 < p.G) ? qg[(size_t)(2 * g2) * d + j] * qscale : 0.f;
-      const float b = (2 * g2 + 1 < p.G) ? qg[(size_t)(2 * g2 + 1) * d + j] * qscale : 0.f;
-      qs[i] = make_float2(a, b);
-    }
-    __syncthreads();
-
-    if (warp < ADA_NL) {
-      // ---------------- logit warps ----------------
-      ptx::mbar_wait(lut_bar, 0);
-      // group-wide prefetch distance: the group's in-flight window (NL tiles
-      // per sharing CTA) plus PF_DIST tiles per CTA beyond it
-      const int pf_dist = (SPHKV_PF_DIST + ADA_NL) * ncta;
-      // the group's first PF tiles, spread over the sharing CTAs' warps
-      for (int t = (blockIdx.x % ncta) * ADA_NL + warp; t < pf_dist && t < ntab;
-           t += ncta * ADA_NL)
-        sh_prefetch(p.tile_tab, tab0, ntab, t, st.pages, st.codes, d, P, TI);
-      // Claims run two tiles ahead and the next tile's table entry + page
-      // descriptor are loaded before the current tile is computed, so no
-      // global round trip sits between two tiles of a warp.
-      int c_next = 0, c_after = 0;
-      if (lane == 0) {
-        c_next = atomicAdd(&p.cursors[gi], 1);
-        c_after = atomicAdd(&p.cursors[gi], 1);
-      }
-      int gt = __shfl_sync(0xffffffffu, c_next, 0);
-      int2 te = make_int2(0, 0);
-      sphkv_page_t pg;
-      if (gt < ntab) {
-        te = p.tile_tab[tab0 + gt];
-        pg = st.pages[te.x];
-      }
-#pragma unroll 1
-      for (;;) {
-        if (gt >= ntab) break;
-        const int gt_n = __shfl_sync(0xffffffffu, c_after, 0);
-        if (lane == 0) c_after = atomicAdd(&p.cursors[gi], 1);  // two ahead
-        int2 te_n = make_int2(0, 0);
-        sphkv_page_t pg_n;
-        if (gt_n < ntab) {
-          te_n = p.tile_tab[tab0 + gt_n];
-          pg_n = st.pages[te_n.x];
-        }
-        int2 pf_te = make_int2(-1, 0);  // L2 prefetch target, issued after the compute
-        if (lane == 0 && gt + pf_dist < ntab) pf_te = p.tile_tab[tab0 + gt + pf_dist];
-        int k = 0;
-        if (lane == 0) {
-          k = atomicAdd(seq_ctr, 1);
-          ring[k % SH_RING] = te;
-          __threadfence_block();
-          ring_seq[k % SH_RING] = k;
-        }
-        k = __shfl_sync(0xffffffffu, k, 0);
-        const int sub = te.y >> 24, ioff = te.y & 0xffffff;
-        const int ti = tier_index(st, pg.tier);
-        float lg[4][2 * GP];
-        ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
-                               p.lut_off[ti], lg);
-        uint32_t valid = 0;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int it = sub * TI + 32 * kk + lane;
-          if (32 * kk + lane < TI && it < pg.count) valid |= 1u << kk;
-        }
-        if (p.logits_dbg != nullptr) {
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 32 * kk + lane) * p.G;
-#pragma unroll
-            for (int g = 0; g < 2 * GP; ++g)
-              if ((valid & (1u << kk)) && g < p.G) dst[g] = lg[kk][g] * (1.0f / kLog2e);
-          }
-        }
-        const int ps = k % ADA_NS;
-        ptx::mbar_wait(&p_empty[ps], ((k / ADA_NS) & 1) ^ 1);
-        write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, p.prows, TI, lane, p.G,
-                            lg, valid);
-        __syncwarp();
-        if (lane == 0) {
-          ptx::mbar_arrive(&p_full[ps]);
-          if (pf_te.x >= 0) {  // prefetch PF tiles ahead in the group's claim order
-            const sphkv_page_t pn = st.pages[pf_te.x];
-            const int sb = pf_te.y >> 24;
-            const uint64_t W4 = (uint64_t)item_words(d, pn.abits) * 128;
-            const int g0 = sb * TI / 32, ng = (TI + 31) / 32;
-            ptx::bulk_prefetch_l2(st.codes + pn.code_off + g0 * W4, (uint32_t)(ng * W4));
-            if (sb == 0) {
-              const uint64_t ab = angle_part_bytes(d, P, pn.abits);
-              ptx::bulk_prefetch_l2(st.codes + pn.code_off + ab,
-                                    (uint32_t)(code_block_bytes(d, P, pn.abits, pn.rbits) - ab));
-            }
-          }
-        }
-        gt = gt_n;
-        te = te_n;
-        pg = pg_n;
-      }
-      if (lane == 0) atomicAdd(done_ctr, 1);
-    } else {
-      // ---------------- PV warp (consumer + V producer) ----------------
-      const uint64_t vpol = ptx::policy_evict_first();
-      const int mt0 = 0, mtn = MT < ADA_MTW ? MT : ADA_MTW;
-      const bool fast_pv = (dvp == 128 && TI == 128 && mtn == ADA_MTW);
-      int issued = 0;
-      PVState<ADA_MTW> s;
-      pv_init(s);
-#pragma unroll 1
-      for (int k = 0;; ++k) {
-        // tile k exists once assigned; the stream ends when every logit warp
-        // has run out of claims and k reached the assigned count
-        int ok = 0;
-        if (lane == 0) {
-          const volatile int* sc = seq_ctr;
-          const volatile int* dc = done_ctr;
-          for (;;) {
-            if (k < *sc) { ok = 1; break; }
-            if (*dc == ADA_NL) { ok = (k < *sc); break; }
-            sh_issue_v(issued, k + ADA_NV, ring, ring_seq, v_full, v_empty, vslots, vbytes,
-                       st.values, P, TI, dvp, vpol);
-            __nanosleep(64);
-          }
-          if (ok)
-            sh_issue_v(issued, k + ADA_NV, ring, ring_seq, v_full, v_empty, vslots, vbytes,
-                       st.values, P, TI, dvp, vpol);
-        }
-        ok = __shfl_sync(0xffffffffu, ok, 0);
-        if (!ok) break;
-        const int vs = k % ADA_NV, ps = k % ADA_NS;
-        ptx::mbar_wait(&v_full[vs], (k / ADA_NV) & 1);
-        ptx::mbar_wait(&p_full[ps], (k / ADA_NS) & 1);
-        if (fast_pv)
-          pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
-                               p.prow_bytes, p.prows, mt0, p.G, lane);
-        else
-          pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
-                           p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane);
-        __syncwarp();
-        if (lane == 0) {
-          ptx::mbar_arrive(&p_empty[ps]);
-          ptx::mbar_arrive(&v_empty[vs]);
-          sh_issue_v(issued, k + 1 + ADA_NV, ring, ring_seq, v_full, v_empty, vslots, vbytes,
-                     st.values, P, TI, dvp, vpol);
-        }
-      }
-      float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
-      pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, true, lane);
-    }
-    __threadfence();
-    __syncthreads();
-    // split count; the CTA completing the group merges it and re-arms the
-    // group's counters for the next launch (every sharing CTA is done)
-    if (threadIdx.x == 0) {
-      s_last = atomicAdd(&p.fz.ctl[gi], 1) == ncta - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-      merge_group_cta(p.fz, p.partials, gi, p.G, st.d_v, s_ml);
-      if (threadIdx.x == 0) p.cursors[gi] = 0;
-    }
-    if (threadIdx.x == 0) {
-      *seq_ctr = 0;
-      *done_ctr = 0;
-    }
-    if (threadIdx.x < SH_RING) ring_seq[threadIdx.x] = -1;
-    __syncthreads();
-  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1233,27 +939,15 @@ static int launch_pdl(Kern kern, const Params& p, int grid, int threads, size_t 
 
 template <int GP>
 static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
-  if (p.tile_tab != nullptr) {
-    auto ks = k_ada_decode_shared<GP>;
-    SPHKV_CUDA_TRY(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    return launch_pdl(ks, p, grid, ADA_THREADS, smem, stream);
-  }
   auto kern = k_ada_decode<GP>;
   SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream);
 }
 
-struct SharedTabs {
-  const int2* tile_tab;
-  const int32_t* tab_begin;
-  int32_t* cursors;
-};
-
 static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
                            const sphkv_unit_t* units, int n_units, float* partials,
                            float* logits_dbg, const int64_t* dbg_offsets, int grid,
-                           const FusedCtl& fz, cudaStream_t stream,
-                           const SharedTabs* sh = nullptr) {
+                           const FusedCtl& fz, cudaStream_t stream) {
   if (!st || !q || !units || !partials) return fail(SPHKV_E_VALUE, "null argument");
   if (G < 1 || G > 8) return fail(SPHKV_E_UNSUPPORTED, "GQA group size %d outside [1, 8]", G);
   if (st->d < 3 || st->d > 256) return fail(SPHKV_E_UNSUPPORTED, "d=%d outside [3, 256]", st->d);
@@ -1278,11 +972,6 @@ static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
   p.logits_dbg = logits_dbg;
   p.dbg_off = dbg_offsets;
   p.fz = fz;
-  if (sh != nullptr) {
-    p.tile_tab = sh->tile_tab;
-    p.tab_begin = sh->tab_begin;
-    p.cursors = sh->cursors;
-  }
   p.TI = st->page_size < ADA_TI ? st->page_size : ADA_TI;
   p.dvp = (st->d_v + 15) / 16 * 16;
   int used = lut_layout(st, p.lut_off);
@@ -1402,25 +1091,6 @@ extern "C" int sphkv_ada_decode_fused(const sphkv_store_t* st, const float* q, i
   int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
   if (rc) return rc;
   return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream);
-}
-
-extern "C" int sphkv_ada_decode_shared(const sphkv_store_t* st, const float* q, int G,
-                                       const sphkv_unit_t* units, int n_units, float* partials,
-                                       const int32_t* slot_group, const int32_t* slot_begin,
-                                       int n_groups, int32_t* ctl, float* out,
-                                       const int32_t* tile_tab, const int32_t* tab_begin,
-                                       int32_t* cursors, int grid, cudaStream_t stream) {
-  if (!slot_group || !tile_tab || !tab_begin || !cursors)
-    return fail(SPHKV_E_VALUE, "shared-cursor decode needs slot_group, tile tables and cursors");
-  if (grid > 0 && n_units > grid)
-    return fail(SPHKV_E_VALUE, "shared-cursor decode runs one unit per CTA (n_units %d > grid %d)",
-                n_units, grid);
-  FusedCtl f;
-  int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, 0);
-  if (rc) return rc;
-  SharedTabs sh{reinterpret_cast<const int2*>(tile_tab), tab_begin, cursors};
-  return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr,
-                         grid > 0 ? grid : n_units, f, stream, &sh);
 }
 
 extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,

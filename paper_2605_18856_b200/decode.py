@@ -62,13 +62,6 @@ def ada_decode(store, q, plan: DecodePlan | None = None, *, out=None, partials=N
         out = torch.empty((ng * G, store.d_v), dtype=torch.float32, device="cuda")
     sp = _lib.stream_ptr(stream)
     # q rows are addressed by absolute group id inside the kernel
-    if logits is None and getattr(plan, "shared", False):  # shared-cursor plan
-        _lib.check(l.sphkv_ada_decode_shared(
-            store.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
-            partials.data_ptr(), plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng,
-            plan.ctl.data_ptr(), out.data_ptr(), plan.tile_tab.data_ptr(),
-            plan.tab_begin.data_ptr(), plan.cursors.data_ptr(), plan.grid, sp))
-        return out
     if logits is None:  # one launch: the last split of each group merges it in-kernel
         _lib.check(l.sphkv_ada_decode_fused(
             store.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,

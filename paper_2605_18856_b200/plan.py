@@ -48,18 +48,6 @@ class DecodePlan:
             sg[:n_slots] = slot_group
         self.slot_group = torch.as_tensor(sg, device="cuda")
         self.ctl = torch.zeros(len(group_ids) + 2, dtype=torch.int32, device="cuda")
-        self.shared = False  # set by plan_store_shared
-
-    def set_shared(self, tile_tab, tab_begin):
-        """Shared-cursor mode (sphkv_ada_decode_shared): per plan group tile
-        table + a zeroed claim cursor per group."""
-        import torch
-
-        self.shared = True
-        self.tile_tab = torch.as_tensor(np.ascontiguousarray(tile_tab, dtype=np.int32),
-                                        device="cuda")
-        self.tab_begin = torch.as_tensor(np.asarray(tab_begin, dtype=np.int32), device="cuda")
-        self.cursors = torch.zeros(len(self.group_ids), dtype=torch.int32, device="cuda")
 
 
 def _page_bytes(rows, tiers, d, d_v, P):
@@ -157,53 +145,6 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
                    lambda g: int(rows["count"][ptr[g, rng[g][0]:rng[g][1]]].sum()),
                    lambda g, s: int(rows["count"][ptr[g, rng[g][0]:s]].sum()) if s > rng[g][0]
                    else 0, dynamic)
-
-
-def plan_store_shared(store, groups=None, grid=SM_COUNT, ranges=None) -> DecodePlan:
-    """Shared-cursor plan: group g gets n_g CTAs (largest remainder on the
-    estimated cost, sum = grid), all covering the whole group; they claim its
-    tiles from one global cursor at run time (sphkv_ada_decode_shared), so
-    per-SM speed differences and cost-model error no longer leave a tail."""
-    n, rows, plen, ptr = store._host()
-    if groups is None:
-        groups = np.arange(store.groups)
-    groups = np.asarray(groups, dtype=np.int64)
-    if ranges is None:
-        ranges = [(0, int(plen[g])) for g in groups]
-    cost = _page_cost(rows, store.d)
-    TI = min(store.page_size, TILE_ITEMS)
-    gcost = np.array([float(cost[ptr[g, rb:re]].sum()) if re > rb else 0.0
-                      for g, (rb, re) in zip(groups, ranges)])
-    grid = max(grid, int((gcost > 0).sum()), 1)
-    if gcost.sum() > 0:
-        share = gcost / gcost.sum() * grid
-        n_g = np.floor(share).astype(np.int64)
-        n_g = np.where((gcost > 0) & (n_g == 0), 1, n_g)
-        rem = grid - int(n_g.sum())
-        for i in np.argsort(-(share - np.floor(share)), kind="stable")[:max(rem, 0)]:
-            n_g[i] += 1
-        while n_g.sum() > grid:  # (the floor-1 bumps can overshoot)
-            n_g[int(np.argmax(n_g))] -= 1
-    else:
-        n_g = np.zeros(len(groups), dtype=np.int64)
-    n_g = np.maximum(n_g, 1)  # every group needs a split (empty groups -> zero rows)
-    pieces, tab, tab_begin = [], [], [0]
-    for g, (rb, re), ng in zip(groups, ranges, n_g):
-        items = 0
-        for pid in ptr[g, rb:re]:
-            c = int(rows["count"][pid])
-            for sub in range(-(-c // TI)):
-                tab.append((int(pid), (sub << 24) | (items + sub * TI)))
-            items += c
-        tab_begin.append(len(tab))
-        for _ in range(int(ng)):
-            pieces.append([0, int(g), rb, re])
-    rng = {int(g): r for g, r in zip(groups, ranges)}
-    plan = _finish(pieces, groups, len(pieces),
-                   lambda g: int(rows["count"][ptr[g, rng[g][0]:rng[g][1]]].sum()),
-                   lambda g, s: 0, dynamic=False)
-    plan.set_shared(np.array(tab, dtype=np.int32).reshape(-1, 2), tab_begin)
-    return plan
 
 
 def split_ranges(page_bytes, world):

@@ -248,14 +248,6 @@ def test_split_merge_equals_single_pass(sk):
     one = sk.ada_decode(st, wl.queries, sk.plan_store(st, grid=2, units_per_cta=1))
     many = sk.ada_decode(st, wl.queries, sk.plan_store(st, grid=148, units_per_cta=4))
     assert torch.allclose(one, many, rtol=2e-5, atol=2e-5)
-    # shared-cursor mode: CTAs of a group claim its tiles from one cursor;
-    # repeated launches reuse the (self re-arming) cursors and counters
-    for grid in (2, 7, 148):
-        plan = sk.plan_store_shared(st, grid=grid)
-        for _ in range(3):
-            shared = sk.ada_decode(st, wl.queries, plan)
-            assert torch.allclose(one, shared, rtol=2e-5, atol=2e-5)
-        assert int(plan.cursors.abs().sum()) == 0 and int(plan.ctl.abs().sum()) == 0
     # repeated fused launches reuse the self re-arming split counters
     plan = sk.plan_store(st, grid=148, units_per_cta=1)
     for _ in range(3):
