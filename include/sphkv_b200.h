@@ -274,6 +274,14 @@ int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const float* q, int 
                              int n_groups, int32_t* ctl, float* out, int dynamic, int grid,
                              cudaStream_t stream);
 
+/* Reconstruct-then-dot negative control (decode.py:195-217):
+ * decode the codes of pages[i] (pointer order) into dense key rows
+ * k~ = r~ * unit(angles), written at rows [item_off[i], item_off[i] + count)
+ * of `out` ([n, d], out_dtype SPHKV_F32 or SPHKV_F16) -- the staging write the
+ * ADA kernel avoids. */
+int sphkv_recon_keys(const sphkv_store_t* st, const int32_t* pages, const int64_t* item_off,
+                     int n_pages, void* out, int out_dtype, cudaStream_t stream);
+
 /* Split-context LSE merge: out fp32 [n_groups*G, d_v]; group g's partials
  * are slots [slot_begin[g], slot_begin[g+1]). Empty splits carry m = -inf. */
 int sphkv_lse_merge(const float* partials, const int32_t* slot_begin,

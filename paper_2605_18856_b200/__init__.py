@@ -16,6 +16,7 @@ from .controller import (ControllerConfig, ControllerFeatures, StateId, StateSco
                          full_best_tier_assignment, protected_mask, score_and_best_tier,
                          score_states)
 from .decode import (AttentionOutput, ada_decode, angle_logits, dense_decode, dense_logits,
+                     recon_logits,
                      logit_drift_bound, lse_merge, softmax_mix, stable_softmax)
 from .plan import DecodePlan, plan_dense, plan_store
 from .store import (DenseStore, PagedStore, ResidentBreakdown, TrafficMeter, dense_mem_estimate,

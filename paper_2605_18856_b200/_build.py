@@ -25,6 +25,7 @@ SOURCES = {
     "decode.cu": [],
     "encode_pack.cu": ["--fmad=false"],
     "rdr.cu": ["--fmad=false"],
+    "recon.cu": [],
 }
 
 

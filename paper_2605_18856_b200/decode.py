@@ -5,7 +5,8 @@ angle  -- `sphkv_ada_decode`: logits straight from radius/angle codes in HBM
           tensor cores, split partials merged by `sphkv_lse_merge`.
 dense  -- `sphkv_dense_decode`: the bf16 paged baseline with the same
           scheduler, page size and partial/merge contract.
-recon  -- the negative control (decode.py:195-217) is SURVEY 8(f) row 4 (next).
+recon  -- the negative control (decode.py:195-217): `sphkv_recon_keys` decodes
+          pages into dense key rows (the staging write), the dot re-reads them.
 
 Batched entry points take device tensors: q fp32 [groups, G, d] with the GQA
 mapping "a reference head is a KV head; each of its G query heads is an
@@ -158,6 +159,46 @@ def angle_logits(q, store, layer, head, query_tier=None) -> np.ndarray:
     return logits[0]
 
 
+def _recon_stage(store, layer, head, stage_dtype="f32"):
+    """Device reconstruction of one head's keys in pointer order (the staging
+    write of the reconstruct-then-dot path); meters the streamed pages and the
+    densification tax exactly as decode.py:195-217 does."""
+    import torch
+
+    l = _lib.require_gpu()
+    pages = [(i, p.count) for i, p in store.stream_pages(layer, head)]  # meters reads
+    live = [(i, c) for i, c in pages if c > 0]
+    if not live:
+        return None, []
+    pids = np.array([i for i, _ in live], dtype=np.int32)
+    counts = np.array([c for _, c in live], dtype=np.int64)
+    off = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+    total = int(counts.sum())
+    dt = {"f32": (torch.float32, _lib.F32), "f16": (torch.float16, _lib.F16)}[stage_dtype]
+    stage = torch.empty((total, store.d), dtype=dt[0], device="cuda")
+    pid_t = torch.as_tensor(pids, device="cuda")
+    off_t = torch.as_tensor(off, device="cuda")
+    _lib.check(l.sphkv_recon_keys(store.cptr, pid_t.data_ptr(), off_t.data_ptr(), len(pids),
+                                  stage.data_ptr(), dt[1], _lib.stream_ptr()))
+    tax = store.d * 2  # dense stage bytes per item, each direction (decode.py:208)
+    store.meter.add_write("dense_k_write", total * tax)
+    store.meter.add_read("dense_k_read", total * tax)
+    return stage, [i for i, _ in live]
+
+
+def recon_logits(q, store, layer, head) -> np.ndarray:
+    """Reconstruct-then-dot negative control (decode.py:195-217): same numbers
+    as angle_logits, plus the dense staging write and re-read."""
+    import torch
+
+    q = np.asarray(q, dtype=np.float64)
+    stage, _ = _recon_stage(store, layer, head)
+    if stage is None:
+        return np.empty(0)
+    qd = torch.as_tensor(q, device="cuda")
+    return (stage.double() @ qd / math.sqrt(store.d)).cpu().numpy()
+
+
 def dense_logits(q, keys) -> np.ndarray:
     """Reference dense logits q . k / sqrt(d) (decode.py:63-69), on the device."""
     import torch
@@ -193,7 +234,15 @@ def _head_attend(path, store, layer, head, q, raw_keys=None, qfeat_pair=None):
     if path not in PATHS:
         raise ValueError(f"unknown path {path!r}")
     if path == "recon":
-        raise ValueError("recon negative control is not on the device path (SURVEY 8(f))")
+        import torch
+
+        stage, pids = _recon_stage(store, layer, head)
+        if stage is None:
+            return np.empty(0), np.zeros(store.d_v), 0, None
+        qd = torch.as_tensor(np.asarray(q, dtype=np.float64), device="cuda")
+        lg = (stage.double() @ qd / math.sqrt(store.d)).cpu().numpy()
+        values = np.concatenate([store.pages[i].values for i in pids])
+        return lg, softmax_mix(lg, values).output, lg.size, None
     if path == "dense":
         import torch
 

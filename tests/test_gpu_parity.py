@@ -456,3 +456,42 @@ def test_compute_features_matches_reference_golden(sk, golden, name):
     np.testing.assert_allclose(feat.u_hat, g[p + "u_hat"], rtol=1e-9, atol=1e-12)
     np.testing.assert_allclose(feat.s_hat, g[p + "s_hat"], rtol=1e-9, atol=1e-12)
     assert abs(feat.r_q - float(g[p + "r_q"])) <= 1e-12 * abs(float(g[p + "r_q"]))
+
+
+def test_recon_negative_control_matches_angle_with_tax(sk):
+    """decode.py:195-217 (reference test_decode.py:100-113): the reconstruct-
+    then-dot path gives the angle path's numbers while the meter carries the
+    exact densification tax n * d * 2 bytes each way on top."""
+    rng = np.random.default_rng(5)
+    L, H, T, d, P = 1, 2, 300, 64, 128
+    tl = [(0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8), (3, 12, 14, 8)]
+    tiers = sk.TierTable(tuple(sk.TierSpec(*t) for t in tl))
+    keys = rng.standard_normal((L, H, T, d))
+    vals = rng.standard_normal((L, H, T, d)).astype(np.float16).astype(np.float64)
+    r, ang = O.encode_batch(keys.reshape(-1, d))
+    r, ang = r.reshape(L, H, T), ang.reshape(L, H, T, d - 1)
+    tier = rng.choice([0, 1, 2, 3], (L, H, T)).astype(np.int16)
+    z = (tier != 0).astype(np.int8)
+    prot = np.zeros((L, H, T), bool)
+
+    def build():
+        return sk.pack_pages_arrays(sk.TierAssignment(z, tier, prot), r, ang, vals, tiers, P)
+
+    st_a, st_r = build(), build()
+    q = rng.standard_normal(d) * 3
+    st_a.meter.reset()
+    st_r.meter.reset()
+    la = sk.angle_logits(q, st_a, 0, 1)
+    lr = sk.recon_logits(q, st_r, 0, 1)
+    n = int(z[0, 1].sum())
+    assert la.shape == lr.shape == (n,)
+    assert np.max(np.abs(la - lr) / np.maximum(1, np.abs(lr))) < 1e-4
+    ost = O.pack_pages(tl, z, tier, prot, r, ang, vals, P)
+    rq, qf = O.query_features(q[None])
+    want, want_out = O.head_attend(ost, 0, 1, rq[0], qf[0])
+    assert np.max(np.abs(lr - want) / np.maximum(1, np.abs(want))) < LOGIT_TOL
+    snap = st_r.meter.snapshot()
+    assert snap["dense_k_write"] == snap["dense_k_read"] == n * d * 2
+    assert st_r.meter.total_bytes == st_a.meter.total_bytes + n * d * 2 * 2
+    lg, out, cnt, _ = sk.decode._head_attend("recon", st_r, 0, 1, q)
+    assert cnt == n and np.max(np.abs(out - want_out)) / np.max(np.abs(want_out)) < OUT_TOL
