@@ -97,9 +97,9 @@ typedef struct {
   uint8_t* protect;           /* [max_pages][P]                               */
   int64_t* token_ids;         /* [max_pages][P]                               */
   uint64_t* counters;         /* [0]=n_pages [1]=code bytes used (device)     */
-  float* lut;                 /* polar (cos, sin) tables, filled by
+  float* lut;                 /* prebuilt (cos, sin) tables, filled by
                                  sphkv_store_build_lut; NULL -> computed in-kernel */
-  int32_t lut_off[SPHKV_MAX_TIERS];  /* float2 offset per tier index, -1 = none */
+  int32_t lut_off[SPHKV_MAX_TIERS];  /* (byte offset << 2) | mode per tier, -1 = none */
 } sphkv_store_t;
 
 /* Dense bf16-K / fp16-V paged store used by the dense baseline kernel

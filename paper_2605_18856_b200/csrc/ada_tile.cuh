@@ -43,49 +43,71 @@ __host__ __device__ constexpr int lut_group(int B) { return B <= 2 ? 4 : (B <= 4
 __host__ __device__ constexpr int lut_entry_bytes(int B) { return lut_group(B) == 1 ? 8 : 16; }
 __host__ __device__ constexpr int lut_rep(int B) { return lut_group(B) == 1 ? 16 : 8; }
 __host__ __device__ constexpr int lut_quad_b_rep() { return 16; }
-__host__ __device__ constexpr int lut_bytes(int B, bool repl) {
+__host__ __device__ constexpr int lut_bytes(int B, int copies) {
   return lut_group(B) == 4
              ? (1 << (4 * B)) * (16 * 8 + 4 * lut_quad_b_rep())  // parts A + B, replicated
-             : (1 << (lut_group(B) * B)) * lut_entry_bytes(B) * (repl ? lut_rep(B) : 1);
+             : (1 << (lut_group(B) * B)) * lut_entry_bytes(B) * copies;
 }
+// table mode (low 2 bits of the encoded descriptor): 0 = one copy, 1 = full
+// replication (lut_rep), 2 = two interleaved copies (single-code tables)
+__host__ __device__ constexpr int lut_copies(int B, int mode) {
+  return mode == 1 ? (lut_group(B) == 4 ? 8 : lut_rep(B)) : (mode == 2 ? 2 : 1);
+}
+__host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
 
-// Encoded per-tier table descriptor: (byte offset << 1) | replicated, or -1.
+// Encoded per-tier table descriptor: (byte offset << 2) | mode, or -1.
+// Placement priority (the budget is shared memory): quad tables (always
+// replicated); full replication of the single-code tiers 5..7 bits, then of
+// the row-pair tiers 3..4; two copies of the wide single-code tiers 8..12
+// (their random gathers conflict ~3x unreplicated; 16 copies do not fit).
 __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n_tiers,
                                                 int off[SPHKV_MAX_TIERS]) {
-  for (int t = 0; t < SPHKV_MAX_TIERS; ++t) off[t] = -1;
-  int minimal = 0;
-  bool repl[SPHKV_MAX_TIERS] = {};
+  int mode[SPHKV_MAX_TIERS];
+  for (int t = 0; t < SPHKV_MAX_TIERS; ++t) {
+    off[t] = -1;
+    mode[t] = 0;
+  }
+  int total = 0;
   for (int t = 1; t < n_tiers; ++t) {
     const int b = tiers[t].angle_bits;
     const bool quad = lut_group(b) == 4;
-    if (b <= LUT_MAX_BITS && minimal + lut_bytes(b, quad) <= LUT_BUDGET_BYTES) {
-      minimal += lut_bytes(b, quad);
+    if (b <= LUT_MAX_BITS && total + lut_bytes(b, quad ? 8 : 1) <= LUT_BUDGET_BYTES) {
+      total += lut_bytes(b, quad ? 8 : 1);
       off[t] = 0;  // has a table; placed below
-      repl[t] = quad;
+      mode[t] = quad ? 1 : 0;
     }
   }
-  int total = minimal;
-  for (int pass_b = 1; pass_b <= LUT_MAX_BITS; ++pass_b)  // narrow tiers first
-    for (int t = 1; t < n_tiers; ++t)
-      if (off[t] == 0 && !repl[t] && tiers[t].angle_bits == pass_b) {
-        const int extra = lut_bytes(pass_b, true) - lut_bytes(pass_b, false);
-        if (total + extra <= LUT_BUDGET_BYTES) {
-          repl[t] = true;
-          total += extra;
+  auto upgrade = [&](int lo, int hi, int m) {
+    for (int b = lo; b <= hi; ++b)
+      for (int t = 1; t < n_tiers; ++t)
+        if (off[t] == 0 && mode[t] == 0 && tiers[t].angle_bits == b) {
+          const int extra = lut_bytes(b, lut_copies(b, m)) - lut_bytes(b, 1);
+          if (total + extra <= LUT_BUDGET_BYTES) {
+            mode[t] = m;
+            total += extra;
+          }
         }
-      }
+  };
+  upgrade(5, 7, 1);
+#ifdef SPHKV_LUT_WIDE_FIRST
+  upgrade(8, LUT_MAX_BITS, 2);
+  upgrade(3, 4, 1);
+#else
+  upgrade(3, 4, 1);
+  upgrade(8, LUT_MAX_BITS, 2);
+#endif
   int used = 0;  // every table size is a multiple of 16 bytes
   for (int t = 1; t < n_tiers; ++t)
     if (off[t] == 0) {
-      off[t] = (used << 1) | (repl[t] ? 1 : 0);
-      used += lut_bytes(tiers[t].angle_bits, repl[t]);
+      off[t] = (used << 2) | mode[t];
+      used += lut_bytes(tiers[t].angle_bits, lut_copies(tiers[t].angle_bits, mode[t]));
     }
   return used;
 }
 
 // Fill one (entry, copy) of a table: tier bits B, entry e, copy r.  Quad
 // tables: copies r < 8 are part A, 8 <= r < 24 part B (copy r - 8).
-__device__ inline void lut_write_entry(uint8_t* dst, int B, bool repl, int e, int r) {
+__device__ inline void lut_write_entry(uint8_t* dst, int B, int copies, int e, int r) {
   const double step = kPi / (double)((1u << B) - 1u);
   if (lut_group(B) == 4) {
     const uint32_t M = (1u << B) - 1u;
@@ -104,7 +126,7 @@ __device__ inline void lut_write_entry(uint8_t* dst, int B, bool repl, int e, in
     }
     return;
   }
-  const int R = repl ? lut_rep(B) : 1;
+  const int R = copies;
   float* out = reinterpret_cast<float*>(dst + ((size_t)e * R + r) * lut_entry_bytes(B));
   if (lut_group(B) == 1) {
     double sn, cs;
@@ -129,11 +151,11 @@ __device__ inline void lut_fill(uint8_t* lut, const sphkv_tier_t* tiers, int n_t
   for (int t = 1; t < n_tiers; ++t) {
     if (enc[t] < 0) continue;
     const int B = tiers[t].angle_bits;
-    const bool repl = enc[t] & 1;
-    const int R = lut_group(B) == 4 ? 8 + lut_quad_b_rep() : (repl ? lut_rep(B) : 1);
+    const int copies = lut_copies(B, enc[t] & 3);
+    const int R = lut_group(B) == 4 ? 8 + lut_quad_b_rep() : copies;
     const int n = (1 << (lut_group(B) * B)) * R;
     for (int i = tid; i < n; i += nthreads)
-      lut_write_entry(lut + (enc[t] >> 1), B, repl, i / R, i % R);
+      lut_write_entry(lut + (enc[t] >> 2), B, copies, i / R, i % R);
   }
 }
 
@@ -344,7 +366,7 @@ __device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::W
 // Specialised tile (B, D known).  A runtime loop over whole periods (codes
 // of the next period requested while the current one is computed), then the
 // remaining polar rows and the circular row with runtime extraction.
-template <int B, int D, int GP, int MODE, bool REPL>
+template <int B, int D, int GP, int MODE, int REP>
 __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int sub, int lane,
                                          const uint8_t* sm, uint32_t qs, uint32_t tb,
                                          uint32_t rbit0, int rb, float rscale,
@@ -354,10 +376,10 @@ __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int s
   constexpr int NP = D - 2;      // polar rows
   constexpr int NFULL = NP / R;  // whole periods of polar rows
   constexpr int EB = (MODE == 2 || MODE == 4) ? 16 : 8;
-  constexpr int STR = REPL ? 7 : ((MODE == 2) ? 4 : 3);
+  constexpr int STR = ilog2c(REP * EB);  // log2 of the entry stride (REP copies)
   const uint32_t qb_off = (MODE == 4) ? (uint32_t)((1 << (4 * B)) * 128) : 0u;
   constexpr uint32_t QR = GP * 8;
-  const uint32_t orv = REPL ? (uint32_t)(lane % (128 / EB)) * EB : 0u;
+  const uint32_t orv = (uint32_t)(lane % REP) * EB;
   const uint32_t* blk = reinterpret_cast<const uint32_t*>(blkb);
   float prod[4];
   ptx::f2 acc[4][GP];
@@ -429,10 +451,11 @@ __device__ __noinline__ void ada_tile_generic(const uint8_t* __restrict__ blk, i
                                               float lg[4][2 * GP]) {
   const int W = item_words(d, B);
   const uint32_t* words = reinterpret_cast<const uint32_t*>(blk);
-  const bool has = lut_enc >= 0, repl = has && (lut_enc & 1);
+  const bool has = lut_enc >= 0;
+  const int copies = has ? lut_copies(B, lut_enc & 3) : 1;
   const int grp = lut_group(B), eb = lut_entry_bytes(B);
-  const uint32_t tbase = has ? (uint32_t)(lut_enc >> 1) + (repl ? (lane % lut_rep(B)) * eb : 0) : 0;
-  const uint32_t stride = repl ? 128u : (uint32_t)eb;
+  const uint32_t tbase = has ? (uint32_t)(lut_enc >> 2) + (lane % copies) * eb : 0;
+  const uint32_t stride = (uint32_t)(copies * eb);
   const uint32_t QR = GP * 8;
   const float pstep = (float)(1.0 / (double)((1u << B) - 1u));
   for (int kk = 0; kk < 4; ++kk) {
@@ -503,7 +526,7 @@ __device__ __noinline__ void ada_tile_generic(const uint8_t* __restrict__ blk, i
 }
 
 // Logits (base 2) of the tile's items sub*128 + 32 k + lane, k < 4, G heads.
-// lut_enc: (table byte offset << 1) | replicated, or -1 (no table).
+// lut_enc: (table byte offset << 2) | mode, or -1 (no table).
 template <int GP>
 __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, int d, int P,
                                                    const sphkv_page_t& pg, int sub, int lane,
@@ -513,31 +536,34 @@ __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, 
   const uint32_t rbit0 = (uint32_t)(angle_part_bytes(d, P, B) * 8);
   const int rb = pg.rbits;
   const float rs = pg.rscale;
-  const bool has = lut_enc >= 0, repl = has && (lut_enc & 1);
-  const uint32_t tb = has ? (uint32_t)(lut_enc >> 1) : 0u;
+  const bool has = lut_enc >= 0;
+  const int mode = has ? (lut_enc & 3) : -1;
+  const uint32_t tb = has ? (uint32_t)(lut_enc >> 2) : 0u;
 #define SPHKV_WI(b, dd, mode, rp) \
   ada_tile_wi<b, dd, GP, mode, rp>(blk, sub, lane, sm, qs, tb, rbit0, rb, rs, lg)
   if (P % 128 != 0) {
     // pages narrower than a tile: generic path (guards items >= P)
   } else if (d == 128) {
-    if (B == 2 && has) { SPHKV_WI(2, 128, 4, true); return; }
-    if (B == 4 && has && repl) { SPHKV_WI(4, 128, 2, true); return; }
-    if (B == 4 && has && !repl) { SPHKV_WI(4, 128, 2, false); return; }
-    if (B == 6 && has && repl) { SPHKV_WI(6, 128, 1, true); return; }
-    if (B == 6 && has && !repl) { SPHKV_WI(6, 128, 1, false); return; }
-    if (B == 7 && has && repl) { SPHKV_WI(7, 128, 1, true); return; }
-    if (B == 7 && has && !repl) { SPHKV_WI(7, 128, 1, false); return; }
+    if (B == 2 && mode == 1) { SPHKV_WI(2, 128, 4, 8); return; }
+    if (B == 4 && mode == 1) { SPHKV_WI(4, 128, 2, 8); return; }
+    if (B == 4 && mode == 0) { SPHKV_WI(4, 128, 2, 1); return; }
+    if (B == 6 && mode == 1) { SPHKV_WI(6, 128, 1, 16); return; }
+    if (B == 6 && mode == 0) { SPHKV_WI(6, 128, 1, 1); return; }
+    if (B == 7 && mode == 1) { SPHKV_WI(7, 128, 1, 16); return; }
+    if (B == 7 && mode == 0) { SPHKV_WI(7, 128, 1, 1); return; }
 #ifdef SPHKV_MUFU12
-    if (B == 12) { SPHKV_WI(12, 128, 3, false); return; }
+    if (B == 12) { SPHKV_WI(12, 128, 3, 1); return; }
 #endif
-    if (B == 12 && has && !repl) { SPHKV_WI(12, 128, 1, false); return; }
-    if (B == 15 && !has) { SPHKV_WI(15, 128, 0, false); return; }
+    if (B == 12 && mode == 2) { SPHKV_WI(12, 128, 1, 2); return; }
+    if (B == 12 && mode == 0) { SPHKV_WI(12, 128, 1, 1); return; }
+    if (B == 15 && !has) { SPHKV_WI(15, 128, 0, 1); return; }
   } else if (d == 64) {
-    if (B == 2 && has) { SPHKV_WI(2, 64, 4, true); return; }
-    if (B == 4 && has && repl) { SPHKV_WI(4, 64, 2, true); return; }
-    if (B == 6 && has && repl) { SPHKV_WI(6, 64, 1, true); return; }
-    if (B == 7 && has && repl) { SPHKV_WI(7, 64, 1, true); return; }
-    if (B == 12 && has && !repl) { SPHKV_WI(12, 64, 1, false); return; }
+    if (B == 2 && mode == 1) { SPHKV_WI(2, 64, 4, 8); return; }
+    if (B == 4 && mode == 1) { SPHKV_WI(4, 64, 2, 8); return; }
+    if (B == 6 && mode == 1) { SPHKV_WI(6, 64, 1, 16); return; }
+    if (B == 7 && mode == 1) { SPHKV_WI(7, 64, 1, 16); return; }
+    if (B == 12 && mode == 2) { SPHKV_WI(12, 64, 1, 2); return; }
+    if (B == 12 && mode == 0) { SPHKV_WI(12, 64, 1, 1); return; }
   }
 #undef SPHKV_WI
   ada_tile_generic<GP>(blk, B, d, P, sub, lane, sm, qs, lut_enc, rbit0, rb, rs, lg);
