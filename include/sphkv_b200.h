@@ -262,6 +262,17 @@ int sphkv_ada_decode_fused(const sphkv_store_t* st, const float* q, int G,
                            int32_t* ctl, float* out, int dynamic, int grid,
                            cudaStream_t stream);
 
+/* sphkv_ada_decode_fused plus the decode-time gate's input: margins fp32
+ * [n_groups * G] = top-1 minus top-2 logit of each (group, query head) over
+ * all of the group's items in natural logit units (+inf with fewer than two
+ * items) -- gate.margin (gate.py:50-56) of the head's logits
+ * (decode.py:433-436).  top2: fp32 scratch [n_slots + 1][G]. */
+int sphkv_ada_decode_margins(const sphkv_store_t* st, const float* q, int G,
+                             const sphkv_unit_t* units, int n_units, float* partials,
+                             const int32_t* slot_group, const int32_t* slot_begin, int n_groups,
+                             int32_t* ctl, float* out, int dynamic, float* top2, float* margins,
+                             int grid, cudaStream_t stream);
+
 /* Dense bf16 paged decode with the same unit/partial contract. */
 int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,
                        const sphkv_unit_t* units, int n_units, float* partials,

@@ -6,7 +6,7 @@ schema.  Compute runs in hand-written sm_100a kernels (libsphkv_b200.so,
 C ABI in include/sphkv_b200.h); there is no CPU fallback.
 """
 
-from . import bitpack, synth
+from . import bitpack, gate, synth
 from ._lib import InfeasibleProtectionError
 from .codec import (AngleCode, RadiusCode, SphericalKey, TierSpec, TierTable, angles_from_unit,
                     cos_from_angles, cos_from_codes, decode_key, encode_batch, encode_key,
@@ -18,6 +18,7 @@ from .controller import (ControllerConfig, ControllerFeatures, StateId, StateSco
 from .decode import (AttentionOutput, ada_decode, angle_logits, dense_decode, dense_logits,
                      recon_logits,
                      logit_drift_bound, lse_merge, softmax_mix, stable_softmax)
+from .gate import GateConfig, GateState, danger_score, gate_step, margin
 from .plan import DecodePlan, plan_dense, plan_store
 from .store import (DenseStore, PagedStore, ResidentBreakdown, TrafficMeter, dense_mem_estimate,
                     pack_device, pack_pages_arrays)

@@ -96,6 +96,8 @@ def _declare(lib):
         "sphkv_lse_merge": (c_int, [vp, vp, i, i, i, vp, vp]),
         "sphkv_lse_merge_ex": (c_int, [vp, vp, i, i64, i, i, i, vp, i, vp]),
         "sphkv_recon_keys": (c_int, [vp, vp, vp, i, vp, i, vp]),
+        "sphkv_ada_decode_margins": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, vp, vp,
+                                             i, vp]),
         "sphkv_ada_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
         "sphkv_dense_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
         "sphkv_partial_floats": (c_int64, [i, i]),

@@ -62,6 +62,8 @@ struct FusedCtl {
   float* out;                 // [n_groups * G, d_v] normalized outputs
   int n_groups;
   int dynamic;                // units claimed from ctl[n_groups] instead of u += grid
+  float* top2;                // [n_slots + 1][G] second-largest logit per split, or NULL
+  float* margins;             // [n_groups * G] top-1 minus top-2 logit (natural units)
 };
 
 struct AdaParams {
@@ -145,10 +147,12 @@ __device__ int build_tiles(const sphkv_store_t& st, const sphkv_unit_t& u, int T
 // Write the fp16 weights of one tile + tile max/sum.  Lane l holds items
 // l + 32 k (k < 4) of the tile; bit k of `valid` says whether item l + 32 k
 // exists.
+// With want2 the header also carries each head's second-largest logit
+// (hdr[16 + g]) for the decode-time gate's top-1/top-2 margin (gate.py:50-56).
 template <int NG>
 __device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int prows, int TI,
                                             int lane, int G, const float lg[4][NG],
-                                            uint32_t valid) {
+                                            uint32_t valid, bool want2 = false) {
   float* hdr = reinterpret_cast<float*>(slot + prows * prow_bytes);
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
@@ -156,6 +160,23 @@ __device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int p
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if (valid & (1u << k)) m = fmaxf(m, lg[k][g]);
+    if (want2) {  // warp top-2 of this head's tile logits
+      float a = -INFINITY, b = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (valid & (1u << k)) {
+          const float v = lg[k][g];
+          b = fmaxf(b, fminf(a, v));
+          a = fmaxf(a, v);
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float a2 = __shfl_xor_sync(0xffffffffu, a, o), b2 = __shfl_xor_sync(0xffffffffu, b, o);
+        b = fmaxf(fminf(a, a2), fmaxf(b, b2));
+        a = fmaxf(a, a2);
+      }
+      if (lane == 0 && g < 8) hdr[16 + g] = b;
+    }
     m = warp_max(m);
     float s = 0.f;
 #pragma unroll
@@ -179,6 +200,7 @@ template <int MTW>
 struct PVState {
   float acc[MTW][4];
   float m[2], l[2];
+  float m2[2];  // running second-largest logit (gate margins)
 };
 
 template <int MTW>
@@ -189,6 +211,18 @@ __device__ __forceinline__ void pv_init(PVState<MTW>& s) {
     for (int r = 0; r < 4; ++r) s.acc[i][r] = 0.f;
   s.m[0] = s.m[1] = -INFINITY;
   s.l[0] = s.l[1] = 0.f;
+  s.m2[0] = s.m2[1] = -INFINITY;
+}
+
+// running top-2 (s.m is the running max) combined with a tile's top-2
+template <int MTW>
+__device__ __forceinline__ void pv_top2(PVState<MTW>& s, const float* hdr, int G, int lane) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int g = 2 * (lane & 3) + h;
+    if (g >= G) continue;
+    s.m2[h] = fmaxf(fminf(s.m[h], hdr[g]), fmaxf(s.m2[h], hdr[16 + g]));
+  }
 }
 
 // One tile of P.V on mma.sync (A = V^T from the swizzled smem tile via
@@ -196,7 +230,7 @@ __device__ __forceinline__ void pv_init(PVState<MTW>& s) {
 template <int MTW>
 __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, const uint8_t* vslot,
                                         int prow_bytes, int prows, int TI, int dvp, int mt0,
-                                        int mtn, int G, int lane) {
+                                        int mtn, int G, int lane, bool want2 = false) {
   float c[MTW][4];
 #pragma unroll
   for (int i = 0; i < MTW; ++i)
@@ -226,6 +260,7 @@ __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, c
     }
   }
   const float* hdr = reinterpret_cast<const float*>(pslot + prows * prow_bytes);
+  if (want2) pv_top2(s, hdr, G, lane);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int g = 2 * (lane & 3) + h;
@@ -250,7 +285,7 @@ __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, c
 template <int MTW>
 __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslot,
                                             const uint8_t* vslot, int prow_bytes, int prows,
-                                            int mt0, int G, int lane) {
+                                            int mt0, int G, int lane, bool want2 = false) {
   float c[MTW][4];
 #pragma unroll
   for (int i = 0; i < MTW; ++i)
@@ -277,6 +312,7 @@ __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslo
     }
   }
   const float* hdr = reinterpret_cast<const float*>(pslot + prows * prow_bytes);
+  if (want2) pv_top2(s, hdr, G, lane);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int g = 2 * (lane & 3) + h;
@@ -297,7 +333,8 @@ __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslo
 // Partial layout per slot: m[G], l[G], acc[G][d_v] (base-2 logit units).
 template <int MTW>
 __device__ __forceinline__ void pv_write(const PVState<MTW>& s, float* part, int G, int d_v,
-                                         int mt0, int mtn, bool write_ml, int lane) {
+                                         int mt0, int mtn, bool write_ml, int lane,
+                                         float* top2 = nullptr) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int g = 2 * (lane & 3) + h;
@@ -305,6 +342,7 @@ __device__ __forceinline__ void pv_write(const PVState<MTW>& s, float* part, int
     if (write_ml && (lane >> 2) == 0) {
       part[g] = s.m[h];
       part[G + g] = s.l[h];
+      if (top2 != nullptr) top2[g] = s.m2[h];
     }
     float* a = part + 2 * G + (size_t)g * d_v;
 #pragma unroll
@@ -368,6 +406,23 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
       s_ml[g] = M;
       s_ml[8 + g] = L;
     }
+    if (f.margins != nullptr) {  // gate margin: top-2 over the union of the splits
+      int cnt = 0;
+      float m2 = -INFINITY;
+      for (int s = b + lane; s < e; s += 32) {
+        const float m = __ldcg(partials + s * stride + g);
+        if (m == M && M != -INFINITY) ++cnt; else m2 = fmaxf(m2, m);
+        m2 = fmaxf(m2, __ldcg(f.top2 + (int64_t)s * G + g));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        m2 = fmaxf(m2, __shfl_xor_sync(0xffffffffu, m2, o));
+      }
+      if (cnt >= 2) m2 = M;
+      if (lane == 0)
+        f.margins[(int64_t)gi * G + g] = (m2 == -INFINITY) ? INFINITY : (M - m2) * 0.69314718055994531f;
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < G * d_v; i += blockDim.x) {
@@ -417,7 +472,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 #ifdef SPHKV_DBG_TIMING
   if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x] = gtimer();
 #endif
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const sphkv_store_t& st = p.st;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float2* lut = reinterpret_cast<float2*>(smem);
@@ -484,8 +539,11 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   };
   // Also independent of the previous grid (it only reads q and writes
   // outputs): the first unit's tile list and its first L2 prefetches.
-  __shared__ int s_flag, s_next;
-  __shared__ float s_ml[16];
+  // scalars of the fused merge / unit queue live after the barriers (no static
+  // __shared__: it would cost a 1 KB-aligned block next to the dynamic region)
+  int& s_flag = *reinterpret_cast<int*>(bars + 2 * ADA_NS + 2 * ADA_NV + 1);
+  int& s_next = *(reinterpret_cast<int*>(bars + 2 * ADA_NS + 2 * ADA_NV + 1) + 1);
+  float* s_ml = reinterpret_cast<float*>(bars + 2 * ADA_NS + 2 * ADA_NV + 2);
   int u = fused_first_unit(p.fz, &s_next);
   if (u < p.n_units && warp == 0) {
     build_tiles(st, p.units[u], TI, tiles, ntiles_s, lane);
@@ -585,7 +643,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         const int ps = gk % ADA_NS;
         ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
         write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, p.prows, TI, lane, p.G, lg,
-                            valid);
+                            valid, p.fz.top2 != nullptr);
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
       }
@@ -611,10 +669,11 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 #ifndef SPHKV_DBG_NOPV  // bottleneck probe: skip the P.V math
         if (fast_pv)
           pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
-                               p.prow_bytes, p.prows, mt0, p.G, lane);
+                               p.prow_bytes, p.prows, mt0, p.G, lane, p.fz.top2 != nullptr);
         else
           pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
-                           p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane);
+                           p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane,
+                           p.fz.top2 != nullptr);
 #endif
         __syncwarp();
         if (lane == 0) {
@@ -624,7 +683,8 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         }
       }
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
-      pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane);
+      pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane,
+                        p.fz.top2 != nullptr ? p.fz.top2 + (size_t)unit.out_slot * p.G : nullptr);
     }
     gbase += nt;
     __syncthreads();
@@ -662,7 +722,7 @@ struct DenseParams {
 };
 
 __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParams p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem[];
   const sphkv_dense_store_t& st = p.st;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* kslots = smem + p.smem_k;
@@ -940,6 +1000,14 @@ static int launch_pdl(Kern kern, const Params& p, int grid, int threads, size_t 
 template <int GP>
 static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
   auto kern = k_ada_decode<GP>;
+  cudaFuncAttributes fa;
+  SPHKV_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+  int dev = 0, optin = 0;
+  SPHKV_CUDA_TRY(cudaGetDevice(&dev));
+  SPHKV_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (smem + fa.sharedSizeBytes > (size_t)optin)
+    return fail(SPHKV_E_UNSUPPORTED, "ADA decode needs %zu B shared memory (+%zu static) > %d",
+                smem, (size_t)fa.sharedSizeBytes, optin);
   SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream);
 }
@@ -990,14 +1058,14 @@ static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
   off = align_up(off + MAX_UNIT_TILES * sizeof(TileEntry) + 16, 128);
   p.prow_bytes = p.TI * 2 + PROW_PAD;
   p.prows = G <= 4 ? 4 : 8;
-  p.pslot_bytes = (int)align_up(p.prows * p.prow_bytes + 64, 128);
+  p.pslot_bytes = (int)align_up(p.prows * p.prow_bytes + 96, 16);  // hdr: m, sum, top-2
   p.smem_p = (uint32_t)off;
   off += (size_t)ADA_NS * p.pslot_bytes;
   off = align_up(off, 1024);
   p.smem_v = (uint32_t)off;
   off += (size_t)ADA_NV * p.TI * p.dvp * 2;
   p.smem_bar = (uint32_t)off;
-  off += (2 * ADA_NS + 2 * ADA_NV + 1) * 8;
+  off += (2 * ADA_NS + 2 * ADA_NV + 1) * 8 + 8 + 64;  // barriers, s_flag/s_next, s_ml[16]
   size_t smem = off;
   if (smem > 227 * 1024) return fail(SPHKV_E_UNSUPPORTED, "ADA smem %zu exceeds 227 KB", smem);
   if (grid <= 0) grid = SM_COUNT;
@@ -1090,6 +1158,22 @@ extern "C" int sphkv_ada_decode_fused(const sphkv_store_t* st, const float* q, i
   FusedCtl f;
   int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
   if (rc) return rc;
+  return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream);
+}
+
+extern "C" int sphkv_ada_decode_margins(const sphkv_store_t* st, const float* q, int G,
+                                        const sphkv_unit_t* units, int n_units, float* partials,
+                                        const int32_t* slot_group, const int32_t* slot_begin,
+                                        int n_groups, int32_t* ctl, float* out, int dynamic,
+                                        float* top2, float* margins, int grid,
+                                        cudaStream_t stream) {
+  if (!slot_group || !top2 || !margins)
+    return fail(SPHKV_E_VALUE, "margins need the fused merge (slot_group), top2 and margins");
+  FusedCtl f;
+  int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
+  if (rc) return rc;
+  f.top2 = top2;
+  f.margins = margins;
   return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream);
 }
 

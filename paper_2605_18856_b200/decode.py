@@ -42,7 +42,7 @@ def _partials(plan, G, d_v):
 
 
 def ada_decode(store, q, plan: DecodePlan | None = None, *, out=None, partials=None,
-               logits=None, stream=None):
+               logits=None, margins=None, stream=None):
     """ADA paged decode over the planned groups.
 
     q: fp32 device tensor [store.groups, G, d] (rows of unplanned groups are
@@ -63,6 +63,15 @@ def ada_decode(store, q, plan: DecodePlan | None = None, *, out=None, partials=N
         out = torch.empty((ng * G, store.d_v), dtype=torch.float32, device="cuda")
     sp = _lib.stream_ptr(stream)
     # q rows are addressed by absolute group id inside the kernel
+    if margins is not None:  # + per (group, q-head) top-1 minus top-2 logit (gate input)
+        assert margins.dtype == torch.float32 and margins.numel() == ng * G
+        top2 = torch.empty((plan.n_slots + 1) * G, dtype=torch.float32, device="cuda")
+        _lib.check(l.sphkv_ada_decode_margins(
+            store.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
+            partials.data_ptr(), plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng,
+            plan.ctl.data_ptr(), out.data_ptr(), int(plan.dynamic), top2.data_ptr(),
+            margins.data_ptr(), plan.grid, sp))
+        return out
     if logits is None:  # one launch: the last split of each group merges it in-kernel
         _lib.check(l.sphkv_ada_decode_fused(
             store.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,

@@ -495,3 +495,40 @@ def test_recon_negative_control_matches_angle_with_tax(sk):
     assert st_r.meter.total_bytes == st_a.meter.total_bytes + n * d * 2 * 2
     lg, out, cnt, _ = sk.decode._head_attend("recon", st_r, 0, 1, q)
     assert cnt == n and np.max(np.abs(out - want_out)) / np.max(np.abs(want_out)) < OUT_TOL
+
+
+def test_decode_margins_for_the_gate(sk):
+    """Per (group, q-head) top-1 minus top-2 logit from the decode kernel (the
+    gate input, gate.py:50-56 on decode.py:433-436 logits) vs the oracle's
+    logits; empty and one-item heads give +inf; outputs are unchanged."""
+    import torch
+    from paper_2605_18856_b200 import gate
+
+    wl = sk.synth.generate(1, 1, 3, 4, 2000, 64, seed=7)
+    tiers = table(sk, [(0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8), (3, 12, 14, 8)])
+    st = sk.PagedStore(tiers, 1, 3, 64, 64, 128, capacity_tokens=2000)
+    n = wl.groups * wl.tokens
+    rng = np.random.default_rng(4)
+    tier = rng.choice([0, 1, 2, 3], n, p=[0.1, 0.4, 0.4, 0.1]).astype(np.int16)
+    tier[wl.tokens: 2 * wl.tokens] = 0      # group 1: empty
+    tier[2 * wl.tokens: 3 * wl.tokens] = 0  # group 2: a single item
+    tier[2 * wl.tokens + 17] = 2
+    radii = torch.empty(n, dtype=torch.float64, device="cuda")
+    from paper_2605_18856_b200 import _lib
+    _lib.check(_lib.lib().sphkv_encode_radii(wl.keys.data_ptr(), _lib.BF16, n, 64,
+                                             radii.data_ptr(), _lib.stream_ptr()))
+    sk.pack_device(st, keys=wl.keys.view(-1, 64), radii=radii, values=wl.values.view(-1, 64),
+                   z=(tier != 0).astype(np.int8), tier=tier, protect=np.zeros(n, np.uint8),
+                   tokens=wl.tokens)
+    for grid in (1, 5, 148):
+        plan = sk.plan_store(st, grid=grid, units_per_cta=1)
+        margins = torch.full((3 * 4,), -1.0, dtype=torch.float32, device="cuda")
+        out = sk.ada_decode(st, wl.queries, plan, margins=margins)
+        ref = sk.ada_decode(st, wl.queries, plan)
+        assert torch.allclose(out, ref, rtol=1e-6, atol=1e-6)
+        m = margins.view(3, 4).cpu().numpy()
+        lg, _ = sk.decode.attend_heads(st, 0, 0, wl.queries[0].double().cpu().numpy())
+        for g in range(4):
+            want = gate.margin(lg[g])
+            assert abs(m[0, g] - want) <= 2e-3 * max(1.0, np.abs(lg[g]).max()), (g, m[0, g], want)
+        assert np.all(np.isinf(m[1])) and np.all(np.isinf(m[2]))
