@@ -30,24 +30,28 @@ class DecodePlan:
         import torch
 
         self.units_host = units
-        self.units = torch.as_tensor(units.view(np.int32).reshape(-1), device="cuda")
+        # plan metadata lives on the device the kernels run on; on a host
+        # without CUDA (planner unit tests) it stays in host memory -- every
+        # decode entry point still requires the GPU (_lib.require_gpu)
+        dev = "cuda" if torch.cuda.is_available() else "cpu"
+        self.units = torch.as_tensor(units.view(np.int32).reshape(-1), device=dev)
         self.n_units = len(units)
         self.slot_begin_host = slot_begin
-        self.slot_begin = torch.as_tensor(slot_begin.astype(np.int32), device="cuda")
+        self.slot_begin = torch.as_tensor(slot_begin.astype(np.int32), device=dev)
         self.n_slots = n_slots
         self.grid = grid
         self.group_items = group_items      # retained items per planned group
         self.group_ids = group_ids          # planned groups, merge order
         self.dbg_offsets_host = dbg_offsets
-        self.dbg_offsets = torch.as_tensor(dbg_offsets, device="cuda")
+        self.dbg_offsets = torch.as_tensor(dbg_offsets, device=dev)
         self.dynamic = dynamic
         # fused in-kernel merge: plan group of every partial slot (+ scratch = -1)
         # and the caller-zeroed control words (sphkv_ada_decode_fused)
         sg = np.full(n_slots + 1, -1, dtype=np.int32)
         if slot_group is not None:
             sg[:n_slots] = slot_group
-        self.slot_group = torch.as_tensor(sg, device="cuda")
-        self.ctl = torch.zeros(len(group_ids) + 2, dtype=torch.int32, device="cuda")
+        self.slot_group = torch.as_tensor(sg, device=dev)
+        self.ctl = torch.zeros(len(group_ids) + 2, dtype=torch.int32, device=dev)
 
 
 def _page_bytes(rows, tiers, d, d_v, P):
@@ -103,16 +107,21 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
     target = max(total // max(grid * units_per_cta, 1), 1)
     pieces = []  # (bytes, group, begin, end, piece index)
     if units_per_cta == 1 and 0 < len(groups) <= grid and total > 0:
+        grid_all = grid
         # one unit per CTA: give each group a share of the grid proportional
         # to its cost (largest remainder) and cut its list at the cost
         # quantiles, so every CTA gets ~total/grid and none gets two pieces
         gcost = np.array([int(pbytes[l].sum()) for l in lists], dtype=np.float64)
+        grid = grid - int((gcost == 0).sum())  # empty groups keep a zero-cost slot of their own
         share = gcost / gcost.sum() * grid
         n_g = np.floor(share).astype(np.int64)
         n_g = np.where((gcost > 0) & (n_g == 0), 1, n_g)
         rem = grid - int(n_g.sum())
         for i in np.argsort(-(share - np.floor(share)), kind="stable")[:max(rem, 0)]:
             n_g[i] += 1
+        while n_g.sum() > max(grid, int((gcost > 0).sum())):  # (the bumps to 1 can overshoot)
+            n_g[int(np.argmax(n_g))] -= 1
+        grid = grid_all
         for g, lst, (rb, _), n in zip(groups, lists, ranges, n_g):
             if len(lst) == 0:
                 pieces.append([0, int(g), rb, rb])
