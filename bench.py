@@ -37,8 +37,11 @@ CONFIGS = {
     # name: (batch, layers, kv_heads, G, tokens, d, description)
     "c1": (1, 1, 8, 4, 8192, 128, "Single-layer ADA+RDR paged decode, Llama-3.1-8B head geometry, B=1, T=8K"),
     "c2": (16, 32, 8, 4, 32768, 128, "Llama-3.1-8B geometry, 32 layers, B=16, T=32K, RDR 30% KV-byte reduction"),
+    "c4": (4, 24, 8, 8, 131072, 64, "gpt-oss-20b geometry (64 Q / 8 KV heads, d=64), 24 layers "
+                                   "alternating sliding-window-128 (even) / full (odd), B=4, T=128K"),
     "c5": (1, 32, 8, 4, 131072, 128, "Single 128K sequence, Llama-3.1-8B geometry, 32 layers, B=1"),
 }
+SWA_CONFIGS = {"c4": 128}  # sliding-window layers (even): only the last W tokens are retained
 PAGE = 256
 REDUCTION = 0.30
 
@@ -162,6 +165,19 @@ def build_workload(cfg_name, rank=0, seed=0, dense=True):
     lut[tier_ids] = torch.arange(len(tiers.tiers), device="cuda")
     gid = torch.arange(groups, device="cuda").repeat_interleave(T)
 
+    swa = SWA_CONFIGS.get(cfg_name)
+    if swa:  # even layers: z = 0 outside the window (no sinks)
+        lay = torch.arange(B * L, device="cuda") % L
+        tok = torch.arange(T, device="cuda")
+        outside = ((lay[:, None, None] % 2 == 0) & (tok[None, None, :] < T - swa)).expand(
+            B * L, H, T).reshape(-1)
+
+    def windowed(z, tier):
+        if swa:
+            z = z.masked_fill(outside.view_as(z), 0)
+            tier = tier.masked_fill(outside.view_as(tier), 0)
+        return z, tier
+
     def resident_of(tier):
         idx = gid * len(tiers.tiers) + lut[tier.view(-1).long()]
         counts = torch.bincount(idx, minlength=groups * len(tiers.tiers)).view(groups, -1)
@@ -176,6 +192,7 @@ def build_workload(cfg_name, rank=0, seed=0, dense=True):
         mid = 0.5 * (lo + hi)
         ta = time.time()
         z, tier = allocate_greedy_device(best, nu, prot, int(mid * dense_key_bits), tiers, d)
+        z, tier = windowed(z, tier)
         torch.cuda.synchronize()
         alloc_ms.append((time.time() - ta) * 1e3)
         res = resident_of(tier)
@@ -240,7 +257,7 @@ def cpu_oracle_sample(W, rank, steps=3, budget_s=20.0):
 
     wl, z, tier = W["wl"], W["z"], W["tier"]
     T, d, G = wl.tokens, wl.d, wl.G
-    g = 0
+    g = wl.heads if wl.layers > 1 else 0  # layer 1, head 0 (full attention when layers alternate)
     keys = wl.keys[g].double().cpu().numpy()
     vals = wl.values[g].double().cpu().numpy()
     r, ang = O.encode_batch(keys)
@@ -355,9 +372,15 @@ def main():
     else:
         plans = layer_plans(st, L, H, B, rank, world, ada_plan)
     n_launch = len(plans)
+    swa = SWA_CONFIGS.get(args.config)
     dplans = [planmod.plan_dense(ds, groups=[(b * L + l) * H + h for b in range(B) for h in range(H)],
-                                 dynamic=args.dynamic)
+                                 dynamic=args.dynamic,
+                                 pages=(ds.n_pages_per_group - (-(-swa // PAGE)), ds.n_pages_per_group)
+                                 if swa and l % 2 == 0 else None)
               for l in range(L)] if not args.no_dense else []
+    if swa:
+        config["sliding_window"] = (f"{swa} tokens on even layers (ADA: z = 0 outside the window; "
+                                    f"dense baseline: the window's last {PAGE}-token page)")
     q = wl.queries
     outs = [torch.empty((len(p.group_ids) * G, d), dtype=torch.float32, device="cuda") for p in plans]
     parts = [sk.decode._partials(p, G, d) for p in plans]

@@ -100,6 +100,8 @@ typedef struct {
   float* lut;                 /* prebuilt (cos, sin) tables, filled by
                                  sphkv_store_build_lut; NULL -> computed in-kernel */
   int32_t lut_off[SPHKV_MAX_TIERS];  /* (byte offset << 2) | mode per tier, -1 = none */
+  int64_t lut_items[SPHKV_MAX_TIERS];  /* items stored per tier index: LUT placement hint
+                                          (all zero = unknown, every tier gets a table) */
 } sphkv_store_t;
 
 /* Dense bf16-K / fp16-V paged store used by the dense baseline kernel

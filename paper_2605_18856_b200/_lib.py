@@ -45,7 +45,8 @@ class CStore(ctypes.Structure):
                 ("pages", c_void_p), ("ptr", c_void_p), ("ptr_len", c_void_p),
                 ("group_last", c_void_p), ("codes", c_void_p), ("values", c_void_p),
                 ("protect", c_void_p), ("token_ids", c_void_p), ("counters", c_void_p),
-                ("lut", c_void_p), ("lut_off", c_int32 * MAX_TIERS)]
+                ("lut", c_void_p), ("lut_off", c_int32 * MAX_TIERS),
+                ("lut_items", ctypes.c_int64 * MAX_TIERS)]
 
 
 class CDenseStore(ctypes.Structure):

@@ -56,13 +56,18 @@ __host__ __device__ constexpr int lut_copies(int B, int mode) {
 __host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
 
 // Encoded per-tier table descriptor: (byte offset << 2) | mode, or -1.
-// Placement priority (the budget is shared memory): quad tables (always
-// replicated); full replication of the single-code tiers 5..7 bits, then of
-// the row-pair tiers 3..4; two copies of the wide single-code tiers 8..12
-// (their random gathers conflict ~3x unreplicated; 16 copies do not fit).
+// With item counts (`items`, per tier index; all zero = unknown) tiers
+// without items get no table and replication goes to the most used tiers
+// first; without them the fixed priority below applies.  Quad tables are
+// always replicated; single-code tiers of 8..12 bits fall back to two copies
+// when full replication (16 copies) does not fit.
 __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n_tiers,
-                                                int off[SPHKV_MAX_TIERS]) {
+                                                int off[SPHKV_MAX_TIERS],
+                                                const int64_t* items = nullptr) {
   int mode[SPHKV_MAX_TIERS];
+  bool known = false;
+  if (items != nullptr)
+    for (int t = 1; t < n_tiers; ++t) known = known || items[t] > 0;
   for (int t = 0; t < SPHKV_MAX_TIERS; ++t) {
     off[t] = -1;
     mode[t] = 0;
@@ -71,31 +76,45 @@ __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n
   for (int t = 1; t < n_tiers; ++t) {
     const int b = tiers[t].angle_bits;
     const bool quad = lut_group(b) == 4;
+    if (known && items[t] == 0) continue;
     if (b <= LUT_MAX_BITS && total + lut_bytes(b, quad ? 8 : 1) <= LUT_BUDGET_BYTES) {
       total += lut_bytes(b, quad ? 8 : 1);
       off[t] = 0;  // has a table; placed below
       mode[t] = quad ? 1 : 0;
     }
   }
-  auto upgrade = [&](int lo, int hi, int m) {
-    for (int b = lo; b <= hi; ++b)
-      for (int t = 1; t < n_tiers; ++t)
-        if (off[t] == 0 && mode[t] == 0 && tiers[t].angle_bits == b) {
-          const int extra = lut_bytes(b, lut_copies(b, m)) - lut_bytes(b, 1);
-          if (total + extra <= LUT_BUDGET_BYTES) {
-            mode[t] = m;
-            total += extra;
-          }
-        }
+  auto upgrade = [&](int t) {
+    const int b = tiers[t].angle_bits;
+    if (off[t] != 0 || mode[t] != 0) return;
+    const int extra = lut_bytes(b, lut_copies(b, 1)) - lut_bytes(b, 1);
+    if (total + extra <= LUT_BUDGET_BYTES) {
+      mode[t] = 1;
+      total += extra;
+    } else if (b >= 8) {
+      const int extra2 = lut_bytes(b, 2) - lut_bytes(b, 1);
+      if (total + extra2 <= LUT_BUDGET_BYTES) {
+        mode[t] = 2;
+        total += extra2;
+      }
+    }
   };
-  upgrade(5, 7, 1);
-#ifdef SPHKV_LUT_WIDE_FIRST
-  upgrade(8, LUT_MAX_BITS, 2);
-  upgrade(3, 4, 1);
-#else
-  upgrade(3, 4, 1);
-  upgrade(8, LUT_MAX_BITS, 2);
-#endif
+  if (known) {  // most items first
+    bool done[SPHKV_MAX_TIERS] = {};
+    for (int k = 1; k < n_tiers; ++k) {
+      int best = -1;
+      for (int t = 1; t < n_tiers; ++t)
+        if (!done[t] && off[t] == 0 && (best < 0 || items[t] > items[best])) best = t;
+      if (best < 0) break;
+      done[best] = true;
+      upgrade(best);
+    }
+  } else {  // fixed priority: single-code 5..7 bits, row-pair 3..4, wide 8..12
+    const int lo[3] = {5, 3, 8}, hi[3] = {7, 4, LUT_MAX_BITS};
+    for (int r = 0; r < 3; ++r)
+      for (int b = lo[r]; b <= hi[r]; ++b)
+        for (int t = 1; t < n_tiers; ++t)
+          if (tiers[t].angle_bits == b) upgrade(t);
+  }
   int used = 0;  // every table size is a multiple of 16 bytes
   for (int t = 1; t < n_tiers; ++t)
     if (off[t] == 0) {

@@ -951,7 +951,7 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 extern "C" int64_t sphkv_partial_floats(int G, int d_v) { return (int64_t)G * (d_v + 2); }
 
 static int lut_layout(const sphkv_store_t* st, int off[SPHKV_MAX_TIERS]) {
-  return lut_layout_tiers(st->tiers, st->n_tiers, off);
+  return lut_layout_tiers(st->tiers, st->n_tiers, off, st->lut_items);
 }
 
 namespace sphkv {

@@ -212,22 +212,25 @@ def merge_gathered(n_groups, world, gathered, G, d_v, out, stream=None):
     return out
 
 
-def plan_dense(dstore, groups=None, grid=SM_COUNT, units_per_cta=2, dynamic=False) -> DecodePlan:
-    """Same planner for the dense baseline store (uniform pages)."""
+def plan_dense(dstore, groups=None, grid=SM_COUNT, units_per_cta=2, dynamic=False,
+               pages=None) -> DecodePlan:
+    """Dense baseline plan; `pages` = (first, end) restricts every group to a
+    page range (sliding-window layers attend to their last pages only)."""
     G = dstore.batch * dstore.layers * dstore.heads
     if groups is None:
         groups = np.arange(G)
     groups = np.asarray(groups, dtype=np.int64)
     npg = dstore.n_pages_per_group
+    p0, p1 = (0, npg) if pages is None else (max(0, int(pages[0])), min(npg, int(pages[1])))
     P = dstore.page_size
     per_page = PAGE_HEADER_BYTES + P * (dstore.d + dstore.d_v) * 2
-    total = len(groups) * npg * per_page
+    total = len(groups) * (p1 - p0) * per_page
     target = max(total // max(grid * units_per_cta, 1), 1)
     pages_per_unit = max(1, min(int(round(target / per_page)), MAX_UNIT_TILES * 64 // P))
     pieces = []
     for g in groups:
-        for s in range(0, max(npg, 1), pages_per_unit):
-            e = min(npg, s + pages_per_unit)
+        for s in range(p0, max(p1, p0 + 1), pages_per_unit):
+            e = min(p1, s + pages_per_unit)
             items = min(e * P, dstore.tokens) - s * P
             pieces.append([max(items, 0) * (dstore.d + dstore.d_v) * 2, int(g), s, e])
     T = dstore.tokens

@@ -290,6 +290,21 @@ class PagedStore:
         self.cstruct = c
         self._build_lut()
 
+    def _refresh_lut(self):
+        """Place the shared-memory tables by the tiers actually stored (items
+        per tier index as the layout hint: absent tiers get no table, the most
+        used tiers are replicated first) and rebuild them when that changes."""
+        n, rows, _, _ = self._host()
+        ids = [t.id for t in self.tiers.tiers]
+        items = [0] * _lib.MAX_TIERS
+        if n:
+            for k, tid in enumerate(ids):
+                items[k] = int(rows["count"][rows["tier"] == tid].sum())
+        if list(self.cstruct.lut_items) != items:
+            for k in range(_lib.MAX_TIERS):
+                self.cstruct.lut_items[k] = items[k]
+            self._build_lut()
+
     def _build_lut(self):
         import torch
 
@@ -709,6 +724,7 @@ def pack_device(store: PagedStore, *, radii, values, z, tier, protect, tokens, a
                                   v.data_ptr(), zz.data_ptr(), tt.data_ptr(), pp.data_ptr(),
                                   tokens, ws.data_ptr(), nbytes, _lib.stream_ptr()))
     store._invalidate()
+    store._refresh_lut()
     return store
 
 
