@@ -3,12 +3,14 @@
 Default workload = config 5 (the north_star target): Llama-3.1-8B attention
 geometry (32 layers, 32 Q / 8 KV heads, d = d_v = 128), one 128K-token
 sequence, P = 256, panel tiers, RDR budget bisected to a 30% resident KV-byte
-reduction vs dense bf16.  A step = one decode token: the ADA decode kernel for
-each of the 32 layers (one launch per layer, CUDA-graph captured) + the LSE
-merge, over inputs already resident in HBM (11+ GB >> 126 MB L2, so no flush
-is needed between steps).  `e2e` repeats the step through the C-ABI call path
-with the step's queries copied from pinned host memory and the attention
-outputs copied back, inside the timed region.
+reduction vs dense bf16.  A step = one decode token: one ADA decode launch per
+layer (32, CUDA-graph captured; the split-context LSE merge is fused into the
+kernel), over inputs already resident in HBM (11+ GB >> 126 MB L2, so no
+flush is needed between steps).  `e2e` repeats the step through the C-ABI
+call path with the step's queries copied from pinned host memory and the
+attention outputs copied back, inside the timed region.  Other workloads:
+--config c1 (one layer, 8K), c2 (B=16, 32K; add --no-dense, the dense copy
+does not fit next to it), c4 (gpt-oss-20b geometry, sliding-window layers).
 
 N > 1 (torchrun): the sequence's page lists are split by page range across
 ranks; partial softmax states are all-gathered over NCCL and LSE-merged on
