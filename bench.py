@@ -350,11 +350,19 @@ def main():
         print(json.dumps(line), flush=True)
         return
 
+    # SPHKV_BENCH_GLOO=1 (debug of the N > 1 path on a single GPU): every rank
+    # on cuda:0, gloo process group, the all-gather staged through host memory
+    gloo_dbg = world > 1 and os.environ.get("SPHKV_BENCH_GLOO") == "1"
+    if gloo_dbg:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo_dbg:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2605_18856_b200 as sk
     from paper_2605_18856_b200 import _lib, plan as planmod
 
@@ -457,7 +465,12 @@ def main():
             for l, p in enumerate(plans):
                 planmod.merge_local_state(p, parts[l], G, d, state[l], stream)
             with torch.cuda.stream(stream):
-                dist.all_gather_into_tensor(gathered.view(-1), state.view(-1))
+                if gloo_dbg:
+                    g_h = torch.empty(gathered.numel(), dtype=torch.float32)
+                    dist.all_gather_into_tensor(g_h, state.view(-1).cpu())
+                    gathered.view(-1).copy_(g_h)
+                else:
+                    dist.all_gather_into_tensor(gathered.view(-1), state.view(-1))
             planmod.merge_gathered(n_launch * ng, world, gathered, G, d, out_all, stream)
 
     # warmup + graph capture of the step (launch-bound loop of 64 kernels)
@@ -490,10 +503,19 @@ def main():
     ms = ev0.elapsed_time(ev1) / args.steps
     clk = clocks.stop()
     if world > 1:
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device="cpu" if gloo_dbg else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     tokens_per_s = B / (ms * 1e-3)
+    if gloo_dbg and rank == 0:  # the split + two-level merge == the single-rank decode
+        ng = len(plans[0].group_ids)
+        worst = 0.0
+        for l in range(L):
+            grp = [(b * L + l) * H + h for b in range(B) for h in range(H)]
+            ref = sk.ada_decode(st, q, planmod.plan_store(st, groups=grp, units_per_cta=1))
+            got = out_all[l * ng * G:(l + 1) * ng * G]
+            worst = max(worst, float((got - ref).abs().max() / ref.abs().max().clamp_min(1e-30)))
+        log(f"N>1 debug: max relative |split merge - single pass| over {L} layers = {worst:.3e}")
 
     # kernel-level timing of the dominant kernel (ADA decode, all layers)
     with torch.cuda.stream(stream):
