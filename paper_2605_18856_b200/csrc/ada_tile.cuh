@@ -279,7 +279,7 @@ __device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::W
                                             uint32_t orv, float (&prod)[4],
                                             ptx::f2 (&acc)[4][GP], uint32_t qb_off = 0) {
   constexpr int R = Period<B>::R, WP = Period<B>::WP;
-  constexpr uint32_t QR = GP * 8;
+  constexpr uint32_t QR = q_row_bytes(GP);
   if constexpr (MODE == 4) {
     // quad-row table: part A at tb, part B at tb + qb_off (4-byte entries, 16
     // copies, 64-byte stride); a trailing row pair uses part A alone
@@ -397,7 +397,7 @@ __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int s
   constexpr int EB = (MODE == 2 || MODE == 4) ? 16 : 8;
   constexpr int STR = ilog2c(REP * EB);  // log2 of the entry stride (REP copies)
   const uint32_t qb_off = (MODE == 4) ? (uint32_t)((1 << (4 * B)) * 128) : 0u;
-  constexpr uint32_t QR = GP * 8;
+  constexpr uint32_t QR = q_row_bytes(GP);
   const uint32_t orv = (uint32_t)(lane % REP) * EB;
   const uint32_t* blk = reinterpret_cast<const uint32_t*>(blkb);
   float prod[4];
@@ -475,7 +475,7 @@ __device__ __noinline__ void ada_tile_generic(const uint8_t* __restrict__ blk, i
   const int grp = lut_group(B), eb = lut_entry_bytes(B);
   const uint32_t tbase = has ? (uint32_t)(lut_enc >> 2) + (lane % copies) * eb : 0;
   const uint32_t stride = (uint32_t)(copies * eb);
-  const uint32_t QR = GP * 8;
+  const uint32_t QR = q_row_bytes(GP);
   const float pstep = (float)(1.0 / (double)((1u << B) - 1u));
   for (int kk = 0; kk < 4; ++kk) {
     const int item = sub * 128 + 32 * kk + lane;

@@ -65,6 +65,10 @@ __host__ __device__ inline uint64_t code_block_bytes(int d, int P, int abits, in
   const uint64_t rbytes = ((uint64_t)P * rbits + 7) / 8;
   return angle_part_bytes(d, P, abits) + ((rbytes + 15) & ~uint64_t(15));
 }
+// Bytes per dimension row of the decode kernels' shared q table: GP packed
+// (q_2g, q_2g+1) float2 pairs, padded to 32 B when GP = 3 so every row start
+// stays 16-byte aligned for the paired 128-bit loads.
+__host__ __device__ constexpr uint32_t q_row_bytes(int GP) { return (GP == 3 ? 4u : (uint32_t)GP) * 8u; }
 // word index (uint32 units from the block start) of string word w of item i
 __host__ __device__ inline uint64_t wi_word(int i, int w, int W) {
   return (((uint64_t)(i >> 5) * (W >> 2) + (w >> 2)) * 32 + (i & 31)) * 4 + (w & 3);

@@ -37,7 +37,7 @@ constexpr int ADA_TI = 128;        // items per tile (4 per lane)
 #endif
 constexpr int ADA_NS = SPHKV_NS;   // P slots
 #ifndef SPHKV_NV
-#define SPHKV_NV 3
+#define SPHKV_NV 2
 #endif
 constexpr int ADA_NV = SPHKV_NV;   // V slots
 #ifndef SPHKV_PF_DIST
@@ -590,7 +590,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       int j = i / GP, g2 = i % GP;
       float a = (2 * g2 < p.G) ? qg[(size_t)(2 * g2) * d + j] * qscale : 0.f;
       float b = (2 * g2 + 1 < p.G) ? qg[(size_t)(2 * g2 + 1) * d + j] * qscale : 0.f;
-      qs[i] = make_float2(a, b);
+      qs[j * (q_row_bytes(GP) / 8) + g2] = make_float2(a, b);
     }
     __syncthreads();
     const int nt = *ntiles_s;
@@ -1053,7 +1053,7 @@ static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
   const int GP = (G + 1) / 2;
   size_t off = align_up((size_t)used, 128);
   p.smem_q = (uint32_t)off;
-  off = align_up(off + (size_t)st->d * GP * 8, 128);
+  off = align_up(off + (size_t)st->d * q_row_bytes(GP), 128);
   p.smem_tiles = (uint32_t)off;
   off = align_up(off + MAX_UNIT_TILES * sizeof(TileEntry) + 16, 128);
   p.prow_bytes = p.TI * 2 + PROW_PAD;

@@ -532,3 +532,31 @@ def test_decode_margins_for_the_gate(sk):
             want = gate.margin(lg[g])
             assert abs(m[0, g] - want) <= 2e-3 * max(1.0, np.abs(lg[g]).max()), (g, m[0, g], want)
         assert np.all(np.isinf(m[1])) and np.all(np.isinf(m[2]))
+
+
+@pytest.mark.parametrize("d,P,G", [(128, 256, 1), (128, 256, 5), (128, 256, 8), (64, 128, 8),
+                                   (64, 128, 3)])
+def test_specialised_tiles_all_gqa_widths(sk, d, P, G):
+    """The specialised tile kernels (d in {64, 128}, P % 128 == 0) for every
+    GQA width class (GP = 1..4: G = 1, 3, 5, 8 -- Llama 4, Qwen 5, gpt-oss 8)
+    and every panel tier, against the oracle on identical inputs."""
+    rng = np.random.default_rng(d * 100 + G)
+    tl = [tuple(t) for t in sk.synth.PANEL_TIERS]
+    tiers = sk.TierTable(tuple(sk.TierSpec(*t) for t in tl))
+    L, H, T = 1, 2, 2 * P + 77
+    keys = rng.standard_normal((L, H, T, d)) * rng.uniform(0.5, 2.0, (L, H, T, 1))
+    vals = rng.standard_normal((L, H, T, d)).astype(np.float16).astype(np.float64)
+    r, ang = O.encode_batch(keys.reshape(-1, d))
+    r, ang = r.reshape(L, H, T), ang.reshape(L, H, T, d - 1)
+    tier = rng.choice([0, 1, 2, 3, 4, 5, 6], (L, H, T)).astype(np.int16)
+    z = (tier != 0).astype(np.int8)
+    prot = np.zeros((L, H, T), bool)
+    st = sk.pack_pages_arrays(sk.TierAssignment(z, tier, prot), r, ang, vals, tiers, P)
+    ost = O.pack_pages(tl, z, tier, prot, r, ang, vals, P)
+    for h in range(H):
+        q = rng.standard_normal((G, d)) * 3
+        lg, out = sk.decode.attend_heads(st, 0, h, q)
+        rq, qf = O.query_features(q)
+        for g in range(G):
+            want_lg, want_out = O.head_attend(ost, 0, h, rq[g], qf[g])
+            assert_attend_close(lg[g], out[g], want_lg, want_out)
