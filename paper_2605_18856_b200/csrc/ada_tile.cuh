@@ -252,6 +252,14 @@ __device__ __forceinline__ void load_item(uint32_t (&w)[W], const uint4* __restr
   }
 }
 
+// Items per lane of a decode tile (a tile is TTI = 32 * TK items: lane l owns
+// items l + 32 k, k < TK).
+#ifndef SPHKV_K
+#define SPHKV_K 4
+#endif
+constexpr int TK = SPHKV_K;
+constexpr int TTI = 32 * TK;
+
 // Rows per "period": the smallest row count whose codes fill whole 32-bit
 // words, so every code's bit offset inside a period is a compile-time
 // constant.  WP = words per period.
@@ -267,17 +275,17 @@ struct Period {
 template <int W>
 __device__ __forceinline__ uint32_t item_word(const uint32_t* __restrict__ blk, int sub, int k,
                                               int lane, int w) {
-  return __ldg(blk + wi_word(sub * 128 + 32 * k + lane, w, W));
+  return __ldg(blk + wi_word(sub * TTI + 32 * k + lane, w, W));
 }
 
 // One period (R rows starting at row r0 = per * R) of the feature recurrence
 // for the lane's 4 items, codes in cw[k][0..WP).  MODE 2: row-pair table,
 // 1: single-code table, 0: sincospif.
 template <int B, int GP, int MODE, int STR, int RR = Period<B>::R>
-__device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::WP],
+__device__ __forceinline__ void period_rows(const uint32_t (&cw)[TK][Period<B>::WP],
                                             const uint8_t* sm, uint32_t qrow0, uint32_t tb,
-                                            uint32_t orv, float (&prod)[4],
-                                            ptx::f2 (&acc)[4][GP], uint32_t qb_off = 0) {
+                                            uint32_t orv, float (&prod)[TK],
+                                            ptx::f2 (&acc)[TK][GP], uint32_t qb_off = 0) {
   constexpr int R = Period<B>::R, WP = Period<B>::WP;
   constexpr uint32_t QR = q_row_bytes(GP);
   if constexpr (MODE == 4) {
@@ -294,7 +302,7 @@ __device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::W
       load_q<GP>(sm, qrow0 + (4 * p + 2) * QR, q2);
       load_q<GP>(sm, qrow0 + (4 * p + 3) * QR, q3);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < TK; ++k) {
         const uint32_t aa = field_addr<4 * B, 4 * p * B, 7, WP>(cw[k], orv);
         const uint32_t ab = field_addr<4 * B, 4 * p * B, 6, WP>(cw[k], orv_b);
         const float4 e = *reinterpret_cast<const float4*>(sm + tb + aa);
@@ -318,7 +326,7 @@ __device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::W
       load_q<GP>(sm, qrow0 + j0 * QR, qa);
       load_q<GP>(sm, qrow0 + (j0 + 1) * QR, qb);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < TK; ++k) {
         const uint32_t a = field_addr<2 * B, j0 * B, 7, WP>(cw[k], orv);
         const float4 e = *reinterpret_cast<const float4*>(sm + tb + a);
         const ptx::f2 f = ptx::f2_mul(ptx::f2_make(prod[k], prod[k]), ptx::f2_make(e.x, e.y));
@@ -338,7 +346,7 @@ __device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::W
       load_q<GP>(sm, qrow0 + (2 * p) * QR, qa);
       load_q<GP>(sm, qrow0 + (2 * p + 1) * QR, qb);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < TK; ++k) {
         const uint32_t a = field_addr<2 * B, 2 * p * B, STR, WP>(cw[k], orv);
         const float4 e = *reinterpret_cast<const float4*>(sm + tb + a);
         const ptx::f2 f = ptx::f2_mul(ptx::f2_make(prod[k], prod[k]), ptx::f2_make(e.x, e.y));
@@ -358,7 +366,7 @@ __device__ __forceinline__ void period_rows(const uint32_t (&cw)[4][Period<B>::W
       ptx::f2 qa[GP];
       load_q<GP>(sm, qrow0 + j * QR, qa);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < TK; ++k) {
         float cs, sn;
         if constexpr (MODE == 1) {
           const uint32_t a = field_addr<B, j * B, STR, WP>(cw[k], orv);
@@ -389,7 +397,7 @@ template <int B, int D, int GP, int MODE, int REP>
 __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int sub, int lane,
                                          const uint8_t* sm, uint32_t qs, uint32_t tb,
                                          uint32_t rbit0, int rb, float rscale,
-                                         float lg[4][2 * GP]) {
+                                         float lg[TK][2 * GP]) {
   constexpr int W = item_words(D, B);
   constexpr int R = Period<B>::R, WP = Period<B>::WP;
   constexpr int NP = D - 2;      // polar rows
@@ -400,30 +408,30 @@ __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int s
   constexpr uint32_t QR = q_row_bytes(GP);
   const uint32_t orv = (uint32_t)(lane % REP) * EB;
   const uint32_t* blk = reinterpret_cast<const uint32_t*>(blkb);
-  float prod[4];
-  ptx::f2 acc[4][GP];
+  float prod[TK];
+  ptx::f2 acc[TK][GP];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < TK; ++k) {
     prod[k] = 1.f;
 #pragma unroll
     for (int g = 0; g < GP; ++g) acc[k][g] = ptx::f2_make(0.f, 0.f);
   }
-  uint32_t cw[4][WP];
+  uint32_t cw[TK][WP];
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < TK; ++k)
 #pragma unroll
     for (int i = 0; i < WP; ++i) cw[k][i] = item_word<W>(blk, sub, k, lane, i);
 #pragma unroll 1
   for (int per = 0; per < NFULL; ++per) {
-    uint32_t nw[4][WP];
+    uint32_t nw[TK][WP];
     const int wn = (per + 1) * WP;  // next period's first word (< W: a tail follows)
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < TK; ++k)
 #pragma unroll
       for (int i = 0; i < WP; ++i) nw[k][i] = item_word<W>(blk, sub, k, lane, min(wn + i, W - 1));
     period_rows<B, GP, MODE, STR>(cw, sm, qs + per * R * QR, tb, orv, prod, acc, qb_off);
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < TK; ++k)
 #pragma unroll
       for (int i = 0; i < WP; ++i) cw[k][i] = nw[k][i];
   }
@@ -437,7 +445,7 @@ __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int s
     load_q<GP>(sm, qs + NP * QR, qa);
     load_q<GP>(sm, qs + (NP + 1) * QR, qb);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < TK; ++k) {
       float sn, cs;
       sincospif((float)field<B, RR * B, WP>(cw[k]) * (1.0f / (float)(1u << (B - 1))), &sn, &cs);
       const float f0 = prod[k] * cs, f1 = prod[k] * sn;
@@ -449,8 +457,8 @@ __device__ __noinline__ void ada_tile_wi(const uint8_t* __restrict__ blkb, int s
     }
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const uint32_t rc = read_bits_g(blk, rbit0 + (uint64_t)(sub * 128 + 32 * k + lane) * rb, rb);
+  for (int k = 0; k < TK; ++k) {
+    const uint32_t rc = read_bits_g(blk, rbit0 + (uint64_t)(sub * TTI + 32 * k + lane) * rb, rb);
     const float rr = (float)rc * rscale;
 #pragma unroll
     for (int g = 0; g < GP; ++g) {
@@ -467,7 +475,7 @@ template <int GP>
 __device__ __noinline__ void ada_tile_generic(const uint8_t* __restrict__ blk, int B, int d,
                                               int P, int sub, int lane, const uint8_t* sm, uint32_t qs,
                                               int lut_enc, uint32_t rbit0, int rb, float rscale,
-                                              float lg[4][2 * GP]) {
+                                              float lg[TK][2 * GP]) {
   const int W = item_words(d, B);
   const uint32_t* words = reinterpret_cast<const uint32_t*>(blk);
   const bool has = lut_enc >= 0;
@@ -477,8 +485,8 @@ __device__ __noinline__ void ada_tile_generic(const uint8_t* __restrict__ blk, i
   const uint32_t stride = (uint32_t)(copies * eb);
   const uint32_t QR = q_row_bytes(GP);
   const float pstep = (float)(1.0 / (double)((1u << B) - 1u));
-  for (int kk = 0; kk < 4; ++kk) {
-    const int item = sub * 128 + 32 * kk + lane;
+  for (int kk = 0; kk < TK; ++kk) {
+    const int item = sub * TTI + 32 * kk + lane;
     if (item >= P) {  // beyond a narrow page: masked by the caller
       for (int g = 0; g < 2 * GP; ++g) lg[kk][g] = 0.f;
       continue;
@@ -550,7 +558,7 @@ template <int GP>
 __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, int d, int P,
                                                    const sphkv_page_t& pg, int sub, int lane,
                                                    const uint8_t* sm, uint32_t qs, int lut_enc,
-                                                   float lg[4][2 * GP]) {
+                                                   float lg[TK][2 * GP]) {
   const uint8_t* blk = codes + pg.code_off;
   const uint32_t rbit0 = (uint32_t)(angle_part_bytes(d, P, B) * 8);
   const int rb = pg.rbits;
@@ -560,7 +568,7 @@ __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, 
   const uint32_t tb = has ? (uint32_t)(lut_enc >> 2) : 0u;
 #define SPHKV_WI(b, dd, mode, rp) \
   ada_tile_wi<b, dd, GP, mode, rp>(blk, sub, lane, sm, qs, tb, rbit0, rb, rs, lg)
-  if (P % 128 != 0) {
+  if (P % TTI != 0) {
     // pages narrower than a tile: generic path (guards items >= P)
   } else if (d == 128) {
     if (B == 2 && mode == 1) { SPHKV_WI(2, 128, 4, 8); return; }

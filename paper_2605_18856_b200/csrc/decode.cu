@@ -31,7 +31,7 @@ constexpr float kLog2e = 1.4426950408889634f;
 #define SPHKV_NL 7
 #endif
 constexpr int ADA_NL = SPHKV_NL;   // logit warps
-constexpr int ADA_TI = 128;        // items per tile (4 per lane)
+constexpr int ADA_TI = TTI;        // items per tile (TK per lane)
 #ifndef SPHKV_NS
 #define SPHKV_NS 12
 #endif
@@ -151,19 +151,19 @@ __device__ int build_tiles(const sphkv_store_t& st, const sphkv_unit_t& u, int T
 // (hdr[16 + g]) for the decode-time gate's top-1/top-2 margin (gate.py:50-56).
 template <int NG>
 __device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int prows, int TI,
-                                            int lane, int G, const float lg[4][NG],
+                                            int lane, int G, const float lg[TK][NG],
                                             uint32_t valid, bool want2 = false) {
   float* hdr = reinterpret_cast<float*>(slot + prows * prow_bytes);
 #pragma unroll
   for (int g = 0; g < NG; ++g) {
     float m = -INFINITY;
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < TK; ++k)
       if (valid & (1u << k)) m = fmaxf(m, lg[k][g]);
     if (want2) {  // warp top-2 of this head's tile logits
       float a = -INFINITY, b = -INFINITY;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < TK; ++k)
         if (valid & (1u << k)) {
           const float v = lg[k][g];
           b = fmaxf(b, fminf(a, v));
@@ -180,7 +180,7 @@ __device__ __forceinline__ void write_pslot(uint8_t* slot, int prow_bytes, int p
     m = warp_max(m);
     float s = 0.f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < TK; ++k) {
       const float e = (valid & (1u << k)) ? exp2f(lg[k][g] - m) : 0.f;
       const __half h = __float2half_rn(e);
       s += __half2float(h);
@@ -301,7 +301,7 @@ __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslo
     va[i] = ptx::smem_u32(vslot) + ((r + (mat >> 1) * 8) * 128 + (chunk ^ r) * 8) * 2;
   }
 #pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
+  for (int ks = 0; ks < ADA_TI / 16; ++ks) {
     uint32_t b0, b1;
     ptx::ldsm_x2(pb + ks * 32, b0, b1);
 #pragma unroll
@@ -617,9 +617,9 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
         const sphkv_page_t pg = st.pages[te.page];
         const int ti = tier_index(st, pg.tier);
-        float lg[4][2 * GP];  // LUT region starts at smem[0]
+        float lg[TK][2 * GP];  // LUT region starts at smem[0]
 #ifdef SPHKV_DBG_NOLOGIT  // bottleneck probe: skip the logit math
-        for (int a_ = 0; a_ < 4; ++a_)
+        for (int a_ = 0; a_ < TK; ++a_)
           for (int b_ = 0; b_ < 2 * GP; ++b_) lg[a_][b_] = (float)(a_ + b_) * 0.01f + (float)ti;
 #else
         ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
@@ -627,13 +627,13 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 #endif
         uint32_t valid = 0;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
+        for (int kk = 0; kk < TK; ++kk) {
           const int it = sub * TI + 32 * kk + lane;
           if (32 * kk + lane < TI && it < pg.count) valid |= 1u << kk;
         }
         if (p.logits_dbg != nullptr) {
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
+          for (int kk = 0; kk < TK; ++kk) {
             float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 32 * kk + lane) * p.G;
 #pragma unroll
             for (int g = 0; g < 2 * GP; ++g)
@@ -660,7 +660,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k, gbase);
       PVState<ADA_MTW> s;
       pv_init(s);
-      const bool fast_pv = (dvp == 128 && TI == 128 && mtn == ADA_MTW);
+      const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
       for (int k = 0; k < nt; ++k) {
         const uint32_t gk = gbase + k;
         const int vs = gk % ADA_NV, ps = gk % ADA_NS;
