@@ -241,6 +241,12 @@ int sphkv_export_streams(const sphkv_store_t* st, int n_pages,
 
 /* ---- decode (decode.py:291-355) ------------------------------------------ */
 
+/* Tile geometry the decode kernels were built with, for the host planner:
+ * items per tile (min(P, this) for narrow pages) and the tile cap of one
+ * work unit (units above it are rejected by the planner, never truncated). */
+int sphkv_ada_tile_items(void);
+int sphkv_unit_tile_cap(void);
+
 /* ADA paged decode: q fp32 [B, L, H*G, d]; per unit writes the partial
  * softmax state (m[G], l[G], acc[G][d_v]) in base-2 logit units to
  * partials[out_slot].  logits_dbg (optional, fp32) receives logits (natural

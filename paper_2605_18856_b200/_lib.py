@@ -83,6 +83,8 @@ def _declare(lib):
         "sphkv_rdr_downtier": (c_int, [vp, vp, vp, i64, vp, i, i, i64, vp, vp, vp, vp]),
         "sphkv_store_reset": (c_int, [vp, vp]),
         "sphkv_lut_floats": (c_int64, [vp]),
+        "sphkv_ada_tile_items": (c_int, []),
+        "sphkv_unit_tile_cap": (c_int, []),
         "sphkv_store_build_lut": (c_int, [vp, vp]),
         "sphkv_pack_pages": (c_int, [vp, vp, i, vp, vp, vp, vp, vp, vp, i, vp, i64, vp]),
         "sphkv_pack_workspace_bytes": (c_int64, [i, i, i, i]),

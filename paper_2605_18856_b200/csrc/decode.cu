@@ -961,6 +961,9 @@ __global__ void k_build_lut(sphkv_store_t st) {
 }
 }  // namespace sphkv
 
+extern "C" int sphkv_ada_tile_items(void) { return ADA_TI; }
+extern "C" int sphkv_unit_tile_cap(void) { return MAX_UNIT_TILES; }
+
 extern "C" int64_t sphkv_lut_floats(const sphkv_store_t* st) {
   int off[SPHKV_MAX_TIERS];
   return lut_layout(st, off) / 4 + 4;

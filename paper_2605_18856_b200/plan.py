@@ -19,8 +19,19 @@ import numpy as np
 from . import _lib
 
 SM_COUNT = 148
-MAX_UNIT_TILES = 512
+MAX_UNIT_TILES = 512   # defaults; the built library's values win (tile_geometry)
 TILE_ITEMS = 128
+_GEOM = None
+
+
+def tile_geometry():
+    """(items per ADA tile, tile cap per unit) of the loaded library
+    (sphkv_ada_tile_items / sphkv_unit_tile_cap)."""
+    global _GEOM
+    if _GEOM is None:
+        l = _lib.lib()
+        _GEOM = (int(l.sphkv_ada_tile_items()), int(l.sphkv_unit_tile_cap()))
+    return _GEOM
 PAGE_HEADER_BYTES = 16
 
 
@@ -60,7 +71,7 @@ def _page_bytes(rows, tiers, d, d_v, P):
     rb = rows["rbits"].astype(np.int64)
     c = rows["count"].astype(np.int64)
     code = (c * (d - 1) * ab + 7) // 8 + (c * rb + 7) // 8
-    ti = min(P, TILE_ITEMS)
+    ti = min(P, tile_geometry()[0])
     return PAGE_HEADER_BYTES + code + 2 * c * d_v, -(-c // ti)
 
 
@@ -132,7 +143,7 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
             cuts = np.minimum(np.maximum.accumulate(cuts), len(lst))
             for s0, e0 in zip(cuts[:-1], cuts[1:]):
                 if e0 > s0:
-                    while int(ptiles[lst[s0:e0]].sum()) > MAX_UNIT_TILES:  # tile cap
+                    while int(ptiles[lst[s0:e0]].sum()) > tile_geometry()[1]:  # tile cap
                         m = s0 + max(1, (e0 - s0) // 2)
                         pieces.append([int(pbytes[lst[s0:m]].sum()), int(g), rb + s0, rb + m])
                         s0 = m
@@ -143,7 +154,7 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
         t = ptiles[lst] if len(lst) else np.zeros(0, np.int64)
         start, acc, tacc = 0, 0, 0
         for k in range(len(lst)):
-            if k > start and (acc + b[k] > target * 1.05 or tacc + t[k] > MAX_UNIT_TILES):
+            if k > start and (acc + b[k] > target * 1.05 or tacc + t[k] > tile_geometry()[1]):
                 pieces.append([acc, int(g), rb + start, rb + k])
                 start, acc, tacc = k, 0, 0
             acc += int(b[k])
