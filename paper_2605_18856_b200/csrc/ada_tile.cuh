@@ -17,7 +17,7 @@ namespace sphkv {
 
 constexpr int LUT_MAX_BITS = 12;
 #ifndef SPHKV_LUT_KB
-#define SPHKV_LUT_KB 108
+#define SPHKV_LUT_KB 124
 #endif
 constexpr int LUT_BUDGET_BYTES = SPHKV_LUT_KB * 1024;
 
