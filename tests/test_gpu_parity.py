@@ -560,3 +560,32 @@ def test_specialised_tiles_all_gqa_widths(sk, d, P, G):
         for g in range(G):
             want_lg, want_out = O.head_attend(ost, 0, h, rq[g], qf[g])
             assert_attend_close(lg[g], out[g], want_lg, want_out)
+
+
+def test_errors_follow_the_reference(sk):
+    """The drop-in raises what the reference raises for the same misuse:
+    KeyError for unknown heads / missing states (store.py:286-287, :442-445),
+    ValueError for a retained state on the drop tier (store.py:450-451) and
+    for a query of the wrong width."""
+    tiers = table(sk, [(0, 0, 0, 0), (1, 4, 6, 0)])
+    L, H, T, d = 1, 2, 64, 8
+    rng = np.random.default_rng(3)
+    r, a = O.encode_batch(rng.standard_normal((L * H * T, d)))
+    r, a = r.reshape(L, H, T), a.reshape(L, H, T, d - 1)
+    vals = rng.standard_normal((L, H, T, d))
+    z = np.ones((L, H, T), np.int8)
+    prot = np.zeros((L, H, T), bool)
+    st = sk.pack_pages_arrays(sk.TierAssignment(z, z.astype(np.int16), prot), r, a, vals,
+                              tiers, 32)
+    with pytest.raises(KeyError):
+        list(st.stream_pages(0, H))
+    with pytest.raises(KeyError):
+        sk.angle_logits(np.ones(d), st, 1, 0)
+    with pytest.raises(ValueError):
+        sk.angle_logits(np.ones(d + 1), st, 0, 0)
+    with pytest.raises(KeyError):  # key arrays shorter than the assignment
+        sk.pack_pages_arrays(sk.TierAssignment(z, z.astype(np.int16), prot), r[:, :, :T - 1],
+                             a[:, :, :T - 1], vals, tiers, 32)
+    with pytest.raises(ValueError):  # retained state on the drop tier
+        sk.pack_pages_arrays(sk.TierAssignment(z, np.zeros((L, H, T), np.int16), prot), r, a,
+                             vals, tiers, 32)
