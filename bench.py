@@ -298,6 +298,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no graphs (for ncu)")
     ap.add_argument("--units-per-cta", type=int, default=1)
+    ap.add_argument("--tail", type=float, default=0.0,
+                    help="fraction of each CTA's share cut into small dynamically claimed units")
     ap.add_argument("--unfused", action="store_true",
                     help="separate LSE-merge launch per layer (default: merge fused in the decode)")
     ap.add_argument("--dynamic", action="store_true",
@@ -373,7 +375,7 @@ def main():
     def ada_plan(s, groups):
         if world == 1:
             return planmod.plan_store(s, groups=groups, units_per_cta=args.units_per_cta,
-                                      dynamic=args.dynamic)
+                                      dynamic=args.dynamic, tail=args.tail)
         return planmod.plan_store_range(s, groups, rank, world, units_per_cta=args.units_per_cta)
 
     if args.fuse_layers:

@@ -398,7 +398,8 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
     float L = 0.f;
     for (int s = b + lane; s < e; s += 32) {
       const float m = __ldcg(partials + s * stride + g);
-      if (m != -INFINITY) L += __ldcg(partials + s * stride + G + g) * exp2f(m - M);
+      const float l = __ldcg(partials + s * stride + G + g);
+      L += (m != -INFINITY) ? l * exp2f(m - M) : 0.f;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
@@ -428,10 +429,14 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
   for (int i = threadIdx.x; i < G * d_v; i += blockDim.x) {
     const int g = i / d_v, j = i % d_v;
     const float M = s_ml[g], L = s_ml[8 + g];
+    // unconditional loads, unrolled: the slots' (m, acc) reads are issued
+    // back to back instead of one L2 round trip per slot
     float a = 0.f;
+#pragma unroll 8
     for (int s = b; s < e; ++s) {
       const float m = __ldcg(partials + s * stride + g);
-      if (m != -INFINITY) a += __ldcg(partials + s * stride + 2 * G + (int64_t)g * d_v + j) * exp2f(m - M);
+      const float v = __ldcg(partials + s * stride + 2 * G + (int64_t)g * d_v + j);
+      a += (m != -INFINITY) ? v * exp2f(m - M) : 0.f;
     }
     f.out[((int64_t)gi * G + g) * d_v + j] = (L > 0.f) ? a / L : 0.f;
   }

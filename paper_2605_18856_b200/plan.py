@@ -99,8 +99,13 @@ def _page_cost(rows, d):
 
 
 def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
-               dynamic=False) -> DecodePlan:
+               dynamic=False, tail=0.0, tail_pieces=2) -> DecodePlan:
     """Plan a decode pass over `groups` (default: every group of the store).
+
+    `tail` (with units_per_cta=1, implies dynamic): each CTA's share is cut
+    into one piece of (1 - tail) of it plus `tail_pieces` small pieces of the
+    rest; CTAs claim the big pieces first, then the small ones as they
+    finish, absorbing the per-CTA speed spread.
 
     `ranges` (optional, one (begin, end) per group) restricts each group to a
     contiguous range of its pointer list -- the page-range split of one
@@ -138,8 +143,14 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
                 pieces.append([0, int(g), rb, rb])
                 continue
             c = np.cumsum(pbytes[lst])
-            cuts = [0] + [int(np.searchsorted(c, c[-1] * k / n, side="left")) + 1
-                          for k in range(1, int(n))] + [len(lst)]
+            if tail > 0:
+                ns = int(n) * int(tail_pieces)
+                fr = [(1.0 - tail) * k / n for k in range(1, int(n) + 1)]
+                fr += [(1.0 - tail) + tail * j / ns for j in range(1, ns)]
+            else:
+                fr = [k / n for k in range(1, int(n))]
+            cuts = [0] + [int(np.searchsorted(c, c[-1] * f, side="left")) + 1
+                          for f in fr] + [len(lst)]
             cuts = np.minimum(np.maximum.accumulate(cuts), len(lst))
             for s0, e0 in zip(cuts[:-1], cuts[1:]):
                 if e0 > s0:
@@ -161,6 +172,7 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
             tacc += int(t[k])
         pieces.append([acc, int(g), rb + start, rb + len(lst)])  # (possibly empty group)
     rng = {int(g): r for g, r in zip(groups, ranges)}
+    dynamic = dynamic or (tail > 0 and units_per_cta == 1)
     return _finish(pieces, groups, grid,
                    lambda g: int(rows["count"][ptr[g, rng[g][0]:rng[g][1]]].sum()),
                    lambda g, s: int(rows["count"][ptr[g, rng[g][0]:s]].sum()) if s > rng[g][0]

@@ -121,3 +121,17 @@ def test_rank_ranges_partition_groups():
                 continue  # padding unit (empty range, scratch slot)
             lo, hi = per_rank[r][groups.index(g)]
             assert lo <= a <= b <= hi
+
+
+def test_tail_pieces_claimed_after_the_big_ones():
+    """tail > 0: one big piece per CTA share first in the claim order, then
+    the small pieces; every page covered exactly once."""
+    st = make_store()
+    plan = planmod.plan_store(st, grid=148, units_per_cta=1, tail=0.2, tail_pieces=2)
+    check_cover(st, plan)
+    assert plan.dynamic
+    c = unit_cost(st, plan)
+    nz = c[c > 0]
+    assert len(nz) > 148
+    big = np.sort(nz)[::-1][:min(148, len(nz) // 3)]
+    assert np.all(c[: len(big)] >= np.sort(c[len(big):]).max() * 0.99)
