@@ -233,11 +233,25 @@ int sphkv_score_append(const double* radii, int groups_per_seq, int heads,
 int sphkv_dense_fill(const sphkv_dense_store_t* st, const void* keys, int key_dtype,
                      const uint16_t* values, cudaStream_t stream);
 
+/* fp64 -> fp16 with one round-to-nearest-even (numpy astype(np.float16),
+ * the SPHKV1 value type, store.py:383); torch's double->half conversion
+ * rounds through fp32 and differs for some inputs. */
+int sphkv_f64_to_f16(const double* in, int64_t n, uint16_t* out, cudaStream_t stream);
+
 /* Reference-format streams of every page: angle stream (stride = count),
  * radius stream, fp16 values un-swizzled [count][d_v], protect bytes.
  * offsets_host give each page's byte offset in `out`. */
 int sphkv_export_streams(const sphkv_store_t* st, int n_pages,
                          const int64_t* offsets, uint8_t* out, cudaStream_t stream);
+
+/* Inverse of sphkv_export_streams (SPHKV1 import, store.py:391-427): with the
+ * page descriptors st->pages[0..n_pages) already set (code_off, count,
+ * group, tier and widths, radius_scale), rebuild each page's device code
+ * block, value rows and protect flags from the same per-page stream layout
+ * (angle stream, radius stream, fp16 values, protect bytes at offsets[pid]);
+ * token ids become -1. */
+int sphkv_import_streams(const sphkv_store_t* st, int n_pages, const int64_t* offsets,
+                         const uint8_t* in, cudaStream_t stream);
 
 /* ---- decode (decode.py:291-355) ------------------------------------------ */
 
@@ -300,6 +314,23 @@ int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const float* q, int 
  * ADA kernel avoids. */
 int sphkv_recon_keys(const sphkv_store_t* st, const int32_t* pages, const int64_t* item_off,
                      int n_pages, void* out, int out_dtype, cudaStream_t stream);
+
+/* The dot's re-read of the staged rows: out[i*G + g] = q_g . stage_i / sqrt(d)
+ * for rows i < n of `stage` ([n, d], SPHKV_F32 or SPHKV_F16), q fp32 [G, d],
+ * G <= 8.  Rows must be whole 16-byte chunks (d*esize % 16 == 0, d <= 256). */
+int sphkv_recon_dot(const void* stage, int stage_dtype, int64_t n, int d, const float* q,
+                    int G, float* out, cudaStream_t stream);
+
+/* dense_logits(q, keys) = keys @ q / sqrt(d) in fp64 (decode.py:63-69):
+ * q [d], keys [n, d] row-major, out [n]. */
+int sphkv_dense_logits(const double* q, const double* keys, int64_t n, int d, double* out,
+                       cudaStream_t stream);
+
+/* Logits of every token of one dense-store group for G <= 8 query heads
+ * (the dense branch of _head_attend, decode.py:302-307, store.py:533-546):
+ * out fp32 [tokens][G] = q_g . k_t / sqrt(d) over the bf16 pages. */
+int sphkv_dense_store_logits(const sphkv_dense_store_t* st, const float* q, int G, int group,
+                             float* out, cudaStream_t stream);
 
 /* Split-context LSE merge: out fp32 [n_groups*G, d_v]; group g's partials
  * are slots [slot_begin[g], slot_begin[g+1]). Empty splits carry m = -inf. */

@@ -26,6 +26,7 @@ SOURCES = {
     "encode_pack.cu": ["--fmad=false"],
     "rdr.cu": ["--fmad=false"],
     "recon.cu": [],
+    "logits.cu": [],
 }
 
 

@@ -93,6 +93,7 @@ def _declare(lib):
         "sphkv_score_append": (c_int, [vp, i, i, vp, vp, d, d, d, d, vp, i, d, i, i64,
                                        vp, vp, vp, vp]),
         "sphkv_export_streams": (c_int, [vp, i, vp, vp, vp]),
+        "sphkv_import_streams": (c_int, [vp, i, vp, vp, vp]),
         "sphkv_dense_fill": (c_int, [vp, vp, i, vp, vp]),
         "sphkv_ada_decode": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp]),
         "sphkv_dense_decode": (c_int, [vp, vp, i, vp, i, vp, i, vp]),
@@ -104,6 +105,10 @@ def _declare(lib):
         "sphkv_ada_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
         "sphkv_dense_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
         "sphkv_partial_floats": (c_int64, [i, i]),
+        "sphkv_f64_to_f16": (c_int, [vp, i64, vp, vp]),
+        "sphkv_recon_dot": (c_int, [vp, i, i64, i, vp, i, vp, vp]),
+        "sphkv_dense_logits": (c_int, [vp, vp, i64, i, vp, vp]),
+        "sphkv_dense_store_logits": (c_int, [vp, vp, i, i, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -177,3 +182,24 @@ def tiers_to_c(tiers) -> "CTier * MAX_TIERS":
             er = tiers.eps_r.get(t.id, 0.0)
         arr[k] = CTier(t.id, t.angle_bits, t.radius_bits, t.meta_bits, et, er)
     return arr
+
+
+def to_f16(x):
+    """Values -> fp16 device tensor with ONE round-to-nearest-even from the
+    source type (numpy astype(np.float16) semantics, store.py:383): numpy
+    input is rounded on the host; a float64 device tensor goes through
+    sphkv_f64_to_f16 (torch's double->half rounds through fp32)."""
+    import torch
+
+    if isinstance(x, torch.Tensor):
+        x = x.to("cuda").contiguous()
+        if x.dtype != torch.float64:
+            return x.to(torch.float16)  # fp32/bf16/fp16: one rounding
+        out = torch.empty(x.shape, dtype=torch.float16, device="cuda")
+        check(require_gpu().sphkv_f64_to_f16(x.data_ptr(), x.numel(), out.data_ptr(),
+                                             stream_ptr()))
+        return out
+    a = np.asarray(x)
+    if a.dtype != np.float16:
+        a = a.astype(np.float64).astype(np.float16)
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")

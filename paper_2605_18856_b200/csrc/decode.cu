@@ -110,15 +110,19 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// Build the unit's tile list (warp 0): returns tile count (also in smem).
-__device__ int build_tiles(const sphkv_store_t& st, const sphkv_unit_t& u, int TI,
-                           TileEntry* tiles, int* ntiles_smem, int lane) {
-  const int* ptr = st.ptr + (size_t)u.group * st.ptr_cap;
-  int nt = 0, items = 0;
-  for (int b = u.ptr_begin; b < u.ptr_end; b += 32) {
+// Build one segment of a unit's tile list (warp 0): whole pages of the
+// pointer range [pb, pe) in order, as many as fit in MAX_UNIT_TILES tiles.
+// Writes the tile count to seg[0] and the first pointer position NOT taken
+// to seg[1] (== pe when the range is done; a unit longer than the cap runs as
+// several segments).  item_base = items of the unit before pb (dbg offsets).
+__device__ void build_tiles(const sphkv_store_t& st, int group, int pb, int pe, int item_base,
+                            int TI, TileEntry* tiles, int* seg, int lane) {
+  const int* ptr = st.ptr + (size_t)group * st.ptr_cap;
+  int nt = 0, items = item_base, next = pe;
+  for (int b = pb; b < pe; b += 32) {
     int pos = b + lane;
     int pid = -1, cnt = 0;
-    if (pos < u.ptr_end) {
+    if (pos < pe) {
       pid = ptr[pos];
       cnt = st.pages[pid].count;
     }
@@ -130,18 +134,30 @@ __device__ int build_tiles(const sphkv_store_t& st, const sphkv_unit_t& u, int T
       int a = __shfl_up_sync(0xffffffffu, ts, o), c = __shfl_up_sync(0xffffffffu, is, o);
       if (lane >= o) { ts += a; is += c; }
     }
+    // pages that fit are a prefix (the scan is monotone)
+    const unsigned fit = __ballot_sync(0xffffffffu, pos < pe && nt + ts <= MAX_UNIT_TILES);
+    const int n_fit = __popc(fit);
     int t0 = nt + ts - t, i0 = items + is - cnt;
-    for (int s = 0; s < t; ++s) {
-      if (t0 + s < MAX_UNIT_TILES) {
+    if ((fit >> lane) & 1u)
+      for (int s = 0; s < t; ++s) {
         tiles[t0 + s].page = pid;
         tiles[t0 + s].sub_off = (s << 24) | (i0 + s * TI);
       }
+    const int last = n_fit - 1;
+    if (n_fit > 0) {
+      nt += __shfl_sync(0xffffffffu, ts, last);
+      items += __shfl_sync(0xffffffffu, is, last);
     }
-    nt += __shfl_sync(0xffffffffu, ts, 31);
-    items += __shfl_sync(0xffffffffu, is, 31);
+    if (n_fit < min(32, pe - b)) {
+      next = b + n_fit;
+      break;
+    }
   }
-  if (lane == 0) *ntiles_smem = nt < MAX_UNIT_TILES ? nt : MAX_UNIT_TILES;
-  return nt;
+  if (lane == 0) {
+    seg[0] = nt;
+    seg[1] = next;
+    seg[2] = items;
+  }
 }
 
 // Write the fp16 weights of one tile + tile max/sum.  Lane l holds items
@@ -382,7 +398,9 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
       last = atomicAdd(&f.ctl[gi], 1) == ns - 1;
     }
     *s_flag = last;
-    if (f.dynamic) *s_next = atomicAdd(&f.ctl[f.n_groups], 1);
+    // the first gridDim.x units are taken statically (blockIdx.x), so queue
+    // claims start at gridDim.x
+    if (f.dynamic) *s_next = atomicAdd(&f.ctl[f.n_groups], 1) + (int)gridDim.x;
   }
   __syncthreads();
   if (!*s_flag) return;
@@ -444,12 +462,11 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
   __syncthreads();
 }
 
-__device__ __forceinline__ int fused_first_unit(const FusedCtl& f, int* s_next) {
-  if (!f.dynamic) return blockIdx.x;
-  if (threadIdx.x == 0) *s_next = atomicAdd(&f.ctl[f.n_groups], 1);
-  __syncthreads();
-  return *s_next;
-}
+// Every CTA's first unit is static (blockIdx.x), dynamic plan or not: the
+// prologue that runs before griddepcontrol.wait (tile list, prefetches) may
+// then touch no control word the previous grid on the stream still uses --
+// queue claims (ctl[n_groups]) happen only after the wait.
+__device__ __forceinline__ int fused_first_unit(const FusedCtl&, int*) { return blockIdx.x; }
 
 __device__ __forceinline__ void fused_kernel_exit(const FusedCtl& f) {
   if (!f.dynamic || threadIdx.x != 0) return;
@@ -483,8 +500,10 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   float2* lut = reinterpret_cast<float2*>(smem);
   float2* qs = reinterpret_cast<float2*>(smem + p.smem_q);
   TileEntry* tiles = reinterpret_cast<TileEntry*>(smem + p.smem_tiles);
-  int* ntiles_s = reinterpret_cast<int*>(smem + p.smem_tiles + MAX_UNIT_TILES * sizeof(TileEntry));
-  int* tile_ctr = ntiles_s + 1;
+  // seg[0] = tiles of the current segment, seg[1] = its end pointer position,
+  // seg[2] = unit items before the next segment; then the tile claim counter
+  int* seg = reinterpret_cast<int*>(smem + p.smem_tiles + MAX_UNIT_TILES * sizeof(TileEntry));
+  int* tile_ctr = seg + 3;
   uint8_t* pslots = smem + p.smem_p;
   uint8_t* vslots = smem + p.smem_v;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
@@ -551,7 +570,8 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   float* s_ml = reinterpret_cast<float*>(bars + 2 * ADA_NS + 2 * ADA_NV + 2);
   int u = fused_first_unit(p.fz, &s_next);
   if (u < p.n_units && warp == 0) {
-    build_tiles(st, p.units[u], TI, tiles, ntiles_s, lane);
+    const sphkv_unit_t u0 = p.units[u];
+    build_tiles(st, u0.group, u0.ptr_begin, u0.ptr_end, 0, TI, tiles, seg, lane);
     if (lane == 0) *tile_ctr = 0;
   }
   __syncthreads();
@@ -570,9 +590,9 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
     ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
   };
   if (u < p.n_units && warp < ADA_NL)
-    for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, *ntiles_s);
+    for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, seg[0]);
   if (u < p.n_units && warp == ADA_NL && lane == 0)
-    for (int k = 0; k < *ntiles_s && k < ADA_NV; ++k) issue_v(k, 0u);
+    for (int k = 0; k < seg[0] && k < ADA_NV; ++k) issue_v(k, 0u);
   ptx::griddep_wait();  // inputs below (q) may come from the previous grid
 #ifdef SPHKV_DBG_TIMING
   if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x] = gtimer();
@@ -583,12 +603,12 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 
   const float qscale = kLog2e * rsqrtf((float)d);
   uint32_t gbase = 0;  // running tile sequence number (barrier phases)
+  const int pw = warp - ADA_NL;  // PV warp index (warp >= ADA_NL)
+  const int mtw = (MT + ADA_NPV - 1) / ADA_NPV;
+  const int mt0 = pw * mtw;
+  const int mtn = max(0, min(mtw, MT - mt0));
   for (; u < p.n_units; first = false) {
     const sphkv_unit_t unit = p.units[u];
-    if (!first && warp == 0) {
-      build_tiles(st, unit, TI, tiles, ntiles_s, lane);
-      if (lane == 0) *tile_ctr = 0;
-    }
     // q rows for this group, prescaled into base-2 logit units, packed pairs
     const float* qg = p.q + (size_t)unit.group * p.G * d;
     for (int i = threadIdx.x; i < d * GP; i += blockDim.x) {
@@ -597,101 +617,112 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       float b = (2 * g2 + 1 < p.G) ? qg[(size_t)(2 * g2 + 1) * d + j] * qscale : 0.f;
       qs[j * (q_row_bytes(GP) / 8) + g2] = make_float2(a, b);
     }
-    __syncthreads();
-    const int nt = *ntiles_s;
-
-    if (warp < ADA_NL) {
-      // ---------------- logit warps ----------------
-      if (!lut_ready) {
-        ptx::mbar_wait(lut_bar, 0);
-        lut_ready = true;
+    PVState<ADA_MTW> s;
+    if (warp >= ADA_NL) pv_init(s);
+    // a unit runs as one or more segments of <= MAX_UNIT_TILES tiles; the
+    // online-softmax state of the PV warps carries across segments
+    for (bool seg_first = true;; seg_first = false) {
+      if (!(first && seg_first) && warp == 0) {
+        const int pb = seg_first ? unit.ptr_begin : seg[1];
+        const int ib = seg_first ? 0 : seg[2];
+        __syncwarp();  // every lane has read seg[] before lane 0 rewrites it
+        build_tiles(st, unit.group, pb, unit.ptr_end, ib, TI, tiles, seg, lane);
+        if (lane == 0) *tile_ctr = 0;
       }
-      // tiles are claimed dynamically (smem counter) to balance the warps;
-      // the P slot of tile k is k % NS whoever computes it.
-#pragma unroll 1
-      if (!first)
-        for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, nt);
-      for (;;) {
-        int k = 0;
-        if (lane == 0) k = atomicAdd(tile_ctr, 1);
-        k = __shfl_sync(0xffffffffu, k, 0);
-        if (k >= nt) break;
-        prefetch_tile(k + SPHKV_PF_DIST, nt);
-        const uint32_t gk = gbase + k;
-        const TileEntry te = tiles[k];
-        const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
-        const sphkv_page_t pg = st.pages[te.page];
-        const int ti = tier_index(st, pg.tier);
-        float lg[TK][2 * GP];  // LUT region starts at smem[0]
-#ifdef SPHKV_DBG_NOLOGIT  // bottleneck probe: skip the logit math
-        for (int a_ = 0; a_ < TK; ++a_)
-          for (int b_ = 0; b_ < 2 * GP; ++b_) lg[a_][b_] = (float)(a_ + b_) * 0.01f + (float)ti;
-#else
-        ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
-                               p.lut_off[ti], lg);
-#endif
-        uint32_t valid = 0;
-#pragma unroll
-        for (int kk = 0; kk < TK; ++kk) {
-          const int it = sub * TI + 32 * kk + lane;
-          if (32 * kk + lane < TI && it < pg.count) valid |= 1u << kk;
+      __syncthreads();
+      const int nt = seg[0], seg_end = seg[1];  // read before warp 0 may rebuild
+
+      if (warp < ADA_NL) {
+        // ---------------- logit warps ----------------
+        if (!lut_ready) {
+          ptx::mbar_wait(lut_bar, 0);
+          lut_ready = true;
         }
-        if (p.logits_dbg != nullptr) {
+        // tiles are claimed dynamically (smem counter) to balance the warps;
+        // the P slot of tile k is k % NS whoever computes it.
+        if (!(first && seg_first))
+          for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, nt);
+#pragma unroll 1
+        for (;;) {
+          int k = 0;
+          if (lane == 0) k = atomicAdd(tile_ctr, 1);
+          k = __shfl_sync(0xffffffffu, k, 0);
+          if (k >= nt) break;
+          prefetch_tile(k + SPHKV_PF_DIST, nt);
+          const uint32_t gk = gbase + k;
+          const TileEntry te = tiles[k];
+          const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
+          const sphkv_page_t pg = st.pages[te.page];
+          const int ti = tier_index(st, pg.tier);
+          float lg[TK][2 * GP];  // LUT region starts at smem[0]
+#ifdef SPHKV_DBG_NOLOGIT  // bottleneck probe: skip the logit math
+          for (int a_ = 0; a_ < TK; ++a_)
+            for (int b_ = 0; b_ < 2 * GP; ++b_) lg[a_][b_] = (float)(a_ + b_) * 0.01f + (float)ti;
+#else
+          ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
+                                 p.lut_off[ti], lg);
+#endif
+          uint32_t valid = 0;
 #pragma unroll
           for (int kk = 0; kk < TK; ++kk) {
-            float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 32 * kk + lane) * p.G;
+            const int it = sub * TI + 32 * kk + lane;
+            if (32 * kk + lane < TI && it < pg.count) valid |= 1u << kk;
+          }
+          if (p.logits_dbg != nullptr) {
 #pragma unroll
-            for (int g = 0; g < 2 * GP; ++g)
-              if ((valid & (1u << kk)) && g < p.G) dst[g] = lg[kk][g] * (1.0f / kLog2e);
+            for (int kk = 0; kk < TK; ++kk) {
+              float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 32 * kk + lane) * p.G;
+#pragma unroll
+              for (int g = 0; g < 2 * GP; ++g)
+                if ((valid & (1u << kk)) && g < p.G) dst[g] = lg[kk][g] * (1.0f / kLog2e);
+            }
+          }
+          const int ps = gk % ADA_NS;
+          ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
+          write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, p.prows, TI, lane, p.G,
+                              lg, valid, p.fz.top2 != nullptr);
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
+        }
+      } else {
+        // ---------------- PV warps ----------------
+        // NPV warps split the d_v m-tiles; all consume every tile in order.
+        // Lane 0 of PV warp 0 is also the V producer: it refills slot vs once
+        // every PV warp has released it (v_empty counts NPV arrivals).
+        if (!(first && seg_first) && pw == 0 && lane == 0)
+          for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k, gbase);
+        const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
+        for (int k = 0; k < nt; ++k) {
+          const uint32_t gk = gbase + k;
+          const int vs = gk % ADA_NV, ps = gk % ADA_NS;
+          ptx::mbar_wait(&v_full[vs], (gk / ADA_NV) & 1);
+          ptx::mbar_wait(&p_full[ps], (gk / ADA_NS) & 1);
+#ifndef SPHKV_DBG_NOPV  // bottleneck probe: skip the P.V math
+          if (fast_pv)
+            pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                                 p.prow_bytes, p.prows, mt0, p.G, lane, p.fz.top2 != nullptr);
+          else
+            pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                             p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane,
+                             p.fz.top2 != nullptr);
+#endif
+          __syncwarp();
+          if (lane == 0) {
+            ptx::mbar_arrive(&p_empty[ps]);
+            ptx::mbar_arrive(&v_empty[vs]);
+            if (pw == 0 && k + ADA_NV < nt) issue_v(k + ADA_NV, gbase);
           }
         }
-        const int ps = gk % ADA_NS;
-        ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
-        write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, p.prows, TI, lane, p.G, lg,
-                            valid, p.fz.top2 != nullptr);
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
       }
-    } else {
-      // ---------------- PV warps ----------------
-      // NPV warps split the d_v m-tiles; all consume every tile in order.
-      // Lane 0 of PV warp 0 is also the V producer: it refills slot vs once
-      // every PV warp has released it (v_empty counts NPV arrivals).
-      const int pw = warp - ADA_NL;
-      const int mtw = (MT + ADA_NPV - 1) / ADA_NPV;
-      const int mt0 = pw * mtw;
-      const int mtn = max(0, min(mtw, MT - mt0));
-      if (!first && pw == 0 && lane == 0)
-        for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k, gbase);
-      PVState<ADA_MTW> s;
-      pv_init(s);
-      const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
-      for (int k = 0; k < nt; ++k) {
-        const uint32_t gk = gbase + k;
-        const int vs = gk % ADA_NV, ps = gk % ADA_NS;
-        ptx::mbar_wait(&v_full[vs], (gk / ADA_NV) & 1);
-        ptx::mbar_wait(&p_full[ps], (gk / ADA_NS) & 1);
-#ifndef SPHKV_DBG_NOPV  // bottleneck probe: skip the P.V math
-        if (fast_pv)
-          pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
-                               p.prow_bytes, p.prows, mt0, p.G, lane, p.fz.top2 != nullptr);
-        else
-          pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
-                           p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane,
-                           p.fz.top2 != nullptr);
-#endif
-        __syncwarp();
-        if (lane == 0) {
-          ptx::mbar_arrive(&p_empty[ps]);
-          ptx::mbar_arrive(&v_empty[vs]);
-          if (pw == 0 && k + ADA_NV < nt) issue_v(k + ADA_NV, gbase);
-        }
-      }
+      gbase += nt;
+      __syncthreads();  // the tile list and seg[] may be rebuilt now
+      if (seg_end >= unit.ptr_end) break;
+    }
+    if (warp >= ADA_NL) {
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
       pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane,
                         p.fz.top2 != nullptr ? p.fz.top2 + (size_t)unit.out_slot * p.G : nullptr);
     }
-    gbase += nt;
     __syncthreads();
     fused_unit_done(p.fz, p.partials, unit.out_slot, p.G, st.d_v, p.n_units, &s_flag, s_ml,
                     &s_next);

@@ -640,6 +640,70 @@ __global__ void k_export(sphkv_store_t st, const int64_t* __restrict__ offsets, 
   for (int i = threadIdx.x; i < n; i += blockDim.x) po[i] = st.protect[(int64_t)pid * P + i];
 }
 
+// import: the inverse of k_export (SPHKV1 from_file, store.py:391-427).  The
+// page descriptors are already in st.pages; `in` holds per page the reference
+// angle stream (stride = count), radius stream, fp16 values [count][d_v] and
+// one protect byte per item at offsets[pid].  One block per page writes the
+// word-interleaved code block, the radius row, the swizzled value rows,
+// protect flags and token ids (-1, as the reference's from_file leaves them).
+__global__ void k_import(sphkv_store_t st, const int64_t* __restrict__ offsets,
+                         const uint8_t* __restrict__ in) {
+  const int pid = blockIdx.x;
+  const sphkv_page_t pg = st.pages[pid];
+  const int d = st.d, P = st.page_size, b = pg.abits, rb = pg.rbits, n = pg.count;
+  const uint8_t* src = in + offsets[pid];
+  uint32_t* words = reinterpret_cast<uint32_t*>(st.codes + pg.code_off);
+  const int W = item_words(d, b);
+  const int64_t nbits = (int64_t)(d - 1) * b;  // valid bits of one item string
+  const int64_t abytes = ((int64_t)n * (d - 1) * b + 7) / 8;
+  const int64_t rbytes = ((int64_t)n * rb + 7) / 8;
+  auto in_bit = [&](int64_t pos) -> uint32_t { return (src[pos >> 3] >> (pos & 7)) & 1u; };
+  const int64_t awords = (int64_t)angle_part_bytes(d, P, b) / 4;
+  for (int64_t k = threadIdx.x; k < awords; k += blockDim.x) {
+    // WI word k -> (item i, string word w)
+    const int64_t quad = k >> 2;
+    const int lane = (int)(quad & 31), w = (int)(((quad >> 5) % (W >> 2)) * 4 + (k & 3));
+    const int i = (int)((quad >> 5) / (W >> 2)) * 32 + lane;
+    uint32_t v = 0;
+    if (i < n)
+      for (int bit = 0; bit < 32; ++bit) {
+        const int64_t sb = (int64_t)w * 32 + bit;
+        if (sb >= nbits) break;
+        const int64_t j = sb / b, cb = sb % b;  // code j of item i, bit cb
+        v |= in_bit((j * n + i) * b + cb) << bit;
+      }
+    words[k] = v;
+  }
+  // radius row: the reference radius stream, bit for bit, zero-padded to P*rb
+  uint32_t* rw = words + awords;
+  const int64_t rwords = ((int64_t)P * rb + 31) / 32;
+  for (int64_t k = threadIdx.x; k < rwords; k += blockDim.x) {
+    uint32_t v = 0;
+    for (int by = 0; by < 4; ++by) {
+      const int64_t byte = k * 4 + by;
+      if (byte < rbytes) v |= (uint32_t)src[abytes + byte] << (8 * by);
+    }
+    rw[k] = v;
+  }
+  const int dv = st.d_v, dvp = (dv + 15) / 16 * 16;
+  const uint8_t* vin = src + abytes + rbytes;
+  uint16_t* vrow = st.values + (int64_t)pid * P * dvp;
+  for (int e = threadIdx.x; e < P * dvp; e += blockDim.x) {
+    const int i = e / dvp, c = e % dvp;
+    uint16_t v = 0;
+    if (i < n && c < dv) {
+      const uint8_t* x = vin + 2 * ((int64_t)i * dv + c);
+      v = (uint16_t)(x[0] | (x[1] << 8));
+    }
+    vrow[vswz(i, c, dvp)] = v;
+  }
+  const uint8_t* pin = vin + 2 * (int64_t)n * dv;
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    st.protect[(int64_t)pid * P + i] = i < n ? pin[i] : 0;
+    st.token_ids[(int64_t)pid * P + i] = -1;
+  }
+}
+
 // dense baseline store: bf16 K and fp16 V pages, swizzled rows
 template <typename T>
 __global__ void k_dense_fill(sphkv_dense_store_t st, const T* __restrict__ keys,
@@ -912,6 +976,17 @@ extern "C" int sphkv_export_streams(const sphkv_store_t* st, int n_pages, const 
   return SPHKV_OK;
 }
 
+extern "C" int sphkv_import_streams(const sphkv_store_t* st, int n_pages, const int64_t* offsets,
+                                    const uint8_t* in, cudaStream_t stream) {
+  if (int e = validate_store(st)) return e;
+  if (n_pages < 0 || n_pages > st->max_pages) return fail(SPHKV_E_CAPACITY, "n_pages %d", n_pages);
+  if (n_pages == 0) return SPHKV_OK;
+  if (!offsets || !in) return fail(SPHKV_E_VALUE, "null argument");
+  k_import<<<n_pages, 256, 0, stream>>>(*st, offsets, in);
+  SPHKV_LAUNCH_CHECK();
+  return SPHKV_OK;
+}
+
 extern "C" int sphkv_dense_fill(const sphkv_dense_store_t* st, const void* keys, int key_dtype,
                                 const uint16_t* values, cudaStream_t stream) {
   if (!st || !keys || !values) return fail(SPHKV_E_VALUE, "null argument");
@@ -922,6 +997,24 @@ extern "C" int sphkv_dense_fill(const sphkv_dense_store_t* st, const void* keys,
     case SPHKV_BF16: k_dense_fill<__nv_bfloat16><<<4 * SM_COUNT, 256, 0, stream>>>(*st, (const __nv_bfloat16*)keys, values); break;
     default: k_dense_fill<__half><<<4 * SM_COUNT, 256, 0, stream>>>(*st, (const __half*)keys, values); break;
   }
+  SPHKV_LAUNCH_CHECK();
+  return SPHKV_OK;
+}
+
+namespace sphkv {
+__global__ void k_f64_to_f16(const double* __restrict__ in, int64_t n, __half* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __double2half(in[i]);  // single rounding, RN-even
+}
+}  // namespace sphkv
+
+extern "C" int sphkv_f64_to_f16(const double* in, int64_t n, uint16_t* out, cudaStream_t stream) {
+  if (n < 0 || (n > 0 && (!in || !out))) return fail(SPHKV_E_VALUE, "null argument");
+  if (n == 0) return SPHKV_OK;
+  const int64_t blocks = (n + 255) / 256;
+  k_f64_to_f16<<<(int)(blocks < 8 * SM_COUNT ? blocks : 8 * SM_COUNT), 256, 0, stream>>>(
+      in, n, reinterpret_cast<__half*>(out));
   SPHKV_LAUNCH_CHECK();
   return SPHKV_OK;
 }

@@ -163,8 +163,7 @@ def angle_logits(q, store, layer, head, query_tier=None) -> np.ndarray:
     if not np.any(qv):
         raise ValueError("query must be nonzero")
     logits, _ = attend_heads(store, layer, head, qv[None])
-    for _ in store.stream_pages(layer, head):  # meter exactly the streamed bytes
-        pass
+    store.meter_stream(layer, head)  # exactly the streamed header, code and value bytes
     return logits[0]
 
 
@@ -195,30 +194,51 @@ def _recon_stage(store, layer, head, stage_dtype="f32"):
     return stage, [i for i, _ in live]
 
 
-def recon_logits(q, store, layer, head) -> np.ndarray:
-    """Reconstruct-then-dot negative control (decode.py:195-217): same numbers
-    as angle_logits, plus the dense staging write and re-read."""
+def _recon_dot(stage, q, d):
+    """The dot's re-read of the staged rows on the device (sphkv_recon_dot):
+    q [G, d] (or [d]) -> logits [n, G] fp32 (natural units)."""
     import torch
 
+    l = _lib.require_gpu()
+    q = np.atleast_2d(np.asarray(q, dtype=np.float64))
+    qd = torch.as_tensor(q, dtype=torch.float32, device="cuda").contiguous()
+    n = stage.shape[0]
+    out = torch.empty((n, q.shape[0]), dtype=torch.float32, device="cuda")
+    dt = _lib.F32 if stage.dtype == torch.float32 else _lib.F16
+    _lib.check(l.sphkv_recon_dot(stage.data_ptr(), dt, n, d, qd.data_ptr(), q.shape[0],
+                                 out.data_ptr(), _lib.stream_ptr()))
+    return out
+
+
+def recon_logits(q, store, layer, head) -> np.ndarray:
+    """Reconstruct-then-dot negative control (decode.py:195-217): same numbers
+    as angle_logits, plus the dense staging write and re-read (both kernels)."""
     q = np.asarray(q, dtype=np.float64)
     stage, _ = _recon_stage(store, layer, head)
     if stage is None:
         return np.empty(0)
-    qd = torch.as_tensor(q, device="cuda")
-    return (stage.double() @ qd / math.sqrt(store.d)).cpu().numpy()
+    return _recon_dot(stage, q, store.d)[:, 0].double().cpu().numpy()
 
 
 def dense_logits(q, keys) -> np.ndarray:
-    """Reference dense logits q . k / sqrt(d) (decode.py:63-69), on the device."""
+    """Reference dense logits keys @ q / sqrt(d) (decode.py:63-69), fp64 on
+    the device (sphkv_dense_logits)."""
     import torch
 
     q = np.asarray(q, dtype=np.float64)
     keys = np.asarray(keys, dtype=np.float64)
     if keys.ndim != 2 or keys.shape[1] != q.shape[0]:
         raise ValueError(f"dimension mismatch: q has {q.shape[0]}, keys {keys.shape}")
+    l = _lib.require_gpu()
+    n, d = keys.shape
+    if n == 0:
+        return np.empty(0)
     qd = torch.as_tensor(q, device="cuda")
-    kd = torch.as_tensor(keys, device="cuda")
-    return (kd @ qd / math.sqrt(q.shape[0])).cpu().numpy()
+    kd = torch.as_tensor(np.ascontiguousarray(keys), device="cuda")
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.check(l.sphkv_dense_logits(qd.data_ptr(), kd.data_ptr(), n, d, out.data_ptr(),
+                                    _lib.stream_ptr()))
+    return out.cpu().numpy()
 
 
 def stable_softmax(logits: np.ndarray) -> np.ndarray:
@@ -239,36 +259,43 @@ def softmax_mix(logits, values) -> AttentionOutput:
 
 
 def _head_attend(path, store, layer, head, q, raw_keys=None, qfeat_pair=None):
-    """(logits, output, n_items, dense_ref_logits) for one head (decode.py:291-355)."""
+    """(logits, output, n_items, dense_ref_logits) for one head (decode.py:291-355).
+
+    Meters as the reference does, once per call: dense -- headers, dense
+    key and value bytes (store.stream_dense); angle / recon -- header, code
+    and value bytes of every listed page, recon adds the densification tax."""
     if path not in PATHS:
         raise ValueError(f"unknown path {path!r}")
     if path == "recon":
-        import torch
-
         stage, pids = _recon_stage(store, layer, head)
         if stage is None:
             return np.empty(0), np.zeros(store.d_v), 0, None
-        qd = torch.as_tensor(np.asarray(q, dtype=np.float64), device="cuda")
-        lg = (stage.double() @ qd / math.sqrt(store.d)).cpu().numpy()
+        lg = _recon_dot(stage, q, store.d)[:, 0].double().cpu().numpy()
         values = np.concatenate([store.pages[i].values for i in pids])
         return lg, softmax_mix(lg, values).output, lg.size, None
     if path == "dense":
         import torch
 
-        l = _lib.require_gpu()
+        if not (0 <= layer < store.layers and 0 <= head < store.heads):
+            raise KeyError(f"unknown (layer, head) = {(layer, head)}")
+        store.meter_dense_stream()
+        if store.tokens == 0:
+            return np.empty(0), np.zeros(store.d_v), 0, None
+        g = (layer * store.heads) + head
         qv = torch.zeros((store.batch * store.layers * store.heads, 1, store.d),
                          dtype=torch.float32, device="cuda")
-        g = (layer * store.heads) + head
         qv[g, 0] = torch.as_tensor(np.asarray(q, dtype=np.float64), device="cuda")
         plan = plan_dense(store, groups=[g], grid=8, units_per_cta=1)
         out = dense_decode(store, qv, plan)
-        return np.empty(0), out[0].double().cpu().numpy(), store.tokens, None
+        lg = store.logits(g, qv[g])[:, 0].double().cpu().numpy()
+        return lg, out[0].double().cpu().numpy(), lg.size, None
     if qfeat_pair is not None:
         r_q, qfeat = qfeat_pair
         qv = float(r_q) * np.asarray(qfeat, dtype=np.float64)
     else:
         qv = np.asarray(q, dtype=np.float64)
     logits, out = attend_heads(store, layer, head, qv[None])
+    store.meter_stream(layer, head)  # header + code + value bytes, batched (decode.py:336-342)
     lg = logits[0]
     ref = None
     if raw_keys is not None and lg.size:

@@ -272,7 +272,11 @@ class PagedStore:
 
     # -- C struct ------------------------------------------------------------
     def _rebuild_cstruct(self):
+        old = getattr(self, "cstruct", None)
         c = _lib.CStore()
+        if old is not None:  # keep the table placement hint across pool growth
+            for k in range(_lib.MAX_TIERS):
+                c.lut_items[k] = old.lut_items[k]
         c.batch, c.layers, c.heads = self.batch, self.layers, self.heads
         c.d, c.d_v, c.page_size = self.d, self.d_v, self.page_size
         c.n_tiers = len(self.tiers.tiers)
@@ -462,7 +466,7 @@ class PagedStore:
               torch.float16: _lib.F16}[k.dtype] if k is not None else 0
         r = dev(radii, torch.float64)
         a = dev(angles, torch.float64)
-        v = dev(values, torch.float16)
+        v = _lib.to_f16(values)
         t = dev(tier_ids, torch.int16)
         p = dev(protect, torch.uint8)
         tk = dev(token_ids, torch.int64)
@@ -473,6 +477,12 @@ class PagedStore:
                                   _lib.ptr(ac), ws.data_ptr(), _lib.stream_ptr()))
         err = int(ws[:4].view(torch.int32).item())
         self._invalidate()
+        if err == 0:  # a tier's first pages may have opened: give it a table
+            sel = t if ac is None else t[ac.bool()]
+            ids = [t_.id for t_ in self.tiers.tiers]
+            new = [int(x) for x in torch.unique(sel).cpu().tolist() if int(x) != DROP_TIER_ID]
+            if any(self.cstruct.lut_items[ids.index(x)] == 0 for x in new if x in ids):
+                self._refresh_lut()
         if err == 3:
             raise RuntimeError("store pool exhausted")
         if err == 4:
@@ -550,6 +560,22 @@ class PagedStore:
             for j in range(page.count):
                 yield (page.tier.id, float(radii[j]), AngleCode(codes[j].copy()), vals[j],
                        bool(prot[j]))
+
+    def meter_stream(self, layer, head, seq=0):
+        """Meter one streamed pass over a head's pages in one batched call
+        (totals identical to stream_pages' per-page reads, decode.py:336-342)."""
+        if not (0 <= layer < self.layers and 0 <= head < self.heads):
+            raise KeyError(f"unknown (layer, head) = {(layer, head)}")
+        n, rows, _, _ = self._host()
+        hdr = code = val = 0
+        for idx in self.group_pages(self._group(layer, head, seq)):
+            r = rows[int(idx)]
+            t = self.tiers.spec_for(int(r["tier"]))
+            a, b, v, *_ = _page_formulas(int(r["count"]), self.page_size, t, self.d, self.d_v)
+            hdr += PAGE_HEADER_BYTES
+            code += a + b
+            val += v
+        self.meter.add_batch((("header", hdr), ("k_codes", code), ("values", val)))
 
     def retained_count(self, layer=None, head=None):
         n, rows, _, _ = self._host()
@@ -651,9 +677,96 @@ class PagedStore:
             f.write(self.to_bytes())
 
     @classmethod
+    def from_bytes(cls, blob: bytes, tiers: TierTable, meter: TrafficMeter | None = None,
+                   *, append_tokens: int = 256) -> "PagedStore":
+        """Load an SPHKV1 snapshot into device pages (store.py:391-427).
+
+        The host parses the headers and the pointer table; the page bytes go
+        to the device in one copy and `sphkv_import_streams` rebuilds the
+        word-interleaved code blocks, swizzled values and protect flags.
+        As in the reference, token ids come back as -1 and values as fp16."""
+        import torch
+
+        mv = memoryview(blob)
+        if bytes(mv[: len(FILE_MAGIC)]) != FILE_MAGIC:
+            raise ValueError("bad magic: not a store snapshot")
+        off = len(FILE_MAGIC)
+        layers, heads, d, d_v, page_size, n_pages = struct.unpack_from("<6I", mv, off)
+        off += 24
+        hdr, spans = [], []
+        for _ in range(n_pages):
+            tid, layer, head, _, count, scale = struct.unpack_from("<BBBBId", mv, off)
+            off += 16
+            t = tiers.spec_for(tid)
+            prot_n, tag_n = (count + 7) // 8, (count * t.meta_bits + 7) // 8
+            a_n, r_n = packed_nbytes(count * (d - 1), t.angle_bits), packed_nbytes(count, t.radius_bits)
+            prot = np.unpackbits(np.frombuffer(mv, np.uint8, prot_n, off))[:count]
+            off += prot_n + tag_n
+            spans.append((off, a_n + r_n + 2 * count * d_v, prot))
+            off += a_n + r_n + 2 * count * d_v
+            hdr.append((t, layer, head, count, scale))
+        groups = layers * heads
+        ptrs = []
+        for _ in range(groups):
+            (n,) = struct.unpack_from("<Q", mv, off)
+            off += 8
+            ptrs.append(np.frombuffer(mv, np.uint64, n, off).astype(np.int64))
+            off += 8 * n
+        per_group = max([len(x) for x in ptrs] + [1])
+        store = cls(tiers, layers, heads, d, d_v, page_size, meter,
+                    capacity_tokens=per_group * page_size, append_tokens=append_tokens)
+        if n_pages + groups > store.max_pages:
+            store._grow(n_pages + groups * (len(tiers.non_drop) + 2))
+        # page table (file order = page ids), code blocks packed back to back
+        rows = np.zeros(n_pages, dtype=_lib.PAGE_DTYPE)
+        code_off = 0
+        for i, (t, layer, head, count, scale) in enumerate(hdr):
+            if layer >= layers or head >= heads or count > page_size:
+                raise ValueError(f"page {i}: header outside the store geometry")
+            rows[i] = (code_off, scale, np.float32(scale / float((1 << t.radius_bits) - 1)), count,
+                       layer * heads + head, t.id, t.angle_bits, t.radius_bits, t.meta_bits)
+            code_off += code_block_bytes(d, page_size, t.angle_bits, t.radius_bits)
+        if code_off > store.code_cap:
+            raise RuntimeError("store pool exhausted")
+        ids = [t.id for t in tiers.tiers]
+        ptr = np.zeros((groups, store.ptr_cap), dtype=np.int32)
+        plen = np.zeros(groups, dtype=np.int32)
+        last = np.full((groups, _lib.MAX_TIERS), -1, dtype=np.int32)
+        for g, lst in enumerate(ptrs):
+            if np.any(lst >= n_pages):
+                raise ValueError("pointer table references a missing page")
+            ptr[g, : len(lst)] = lst
+            plen[g] = len(lst)
+            for idx in lst:  # store.py:423-426
+                last[g, ids.index(int(rows[idx]["tier"]))] = idx
+        # stream blob in the export layout: angle | radius | values | protect bytes
+        offs = np.zeros(n_pages + 1, dtype=np.int64)
+        for i, (_, ln, prot) in enumerate(spans):
+            offs[i + 1] = offs[i] + ln + len(prot)
+        buf = np.zeros(int(offs[-1]) + 16, dtype=np.uint8)
+        for i, (o, ln, prot) in enumerate(spans):
+            buf[offs[i]: offs[i] + ln] = np.frombuffer(mv, np.uint8, ln, o)
+            buf[offs[i] + ln: offs[i + 1]] = prot
+        dev = "cuda"
+        store.t_pages[: n_pages * 32] = torch.as_tensor(rows.view(np.uint8), device=dev)
+        store.t_ptr.view(groups, store.ptr_cap).copy_(torch.as_tensor(ptr, device=dev))
+        store.t_ptr_len.copy_(torch.as_tensor(plen, device=dev))
+        store.t_group_last.copy_(torch.as_tensor(last.reshape(-1), device=dev))
+        store.t_counters[0] = n_pages
+        store.t_counters[1] = code_off
+        l = _lib.require_gpu()
+        blob_d = torch.as_tensor(buf, device=dev)
+        offs_d = torch.as_tensor(offs[:-1], device=dev)
+        _lib.check(l.sphkv_import_streams(store.cptr, n_pages, offs_d.data_ptr(),
+                                          blob_d.data_ptr(), _lib.stream_ptr()))
+        store._invalidate()
+        store._refresh_lut()
+        return store
+
+    @classmethod
     def from_file(cls, path: str, tiers: TierTable) -> "PagedStore":
-        raise NotImplementedError(
-            "SPHKV1 import into device pages is SURVEY 8(f) row 3 (next); export is supported")
+        with open(path, "rb") as f:
+            return cls.from_bytes(f.read(), tiers)
 
 
 def pack_pages_arrays(assignment, radii, angles, values, tiers: TierTable, page_size: int,
@@ -714,7 +827,7 @@ def pack_device(store: PagedStore, *, radii, values, z, tier, protect, tokens, a
               torch.float16: _lib.F16}[k.dtype]
     r = dev(radii, torch.float64)
     a = dev(angles, torch.float64)
-    v = dev(values, torch.float16)
+    v = _lib.to_f16(values)
     zz = dev(z, torch.int8)
     tt = dev(tier, torch.int16)
     pp = dev(protect, torch.uint8)
@@ -749,7 +862,7 @@ class DenseStore:
         k = keys if isinstance(keys, torch.Tensor) else torch.as_tensor(np.asarray(keys), device="cuda")
         v = values if isinstance(values, torch.Tensor) else torch.as_tensor(np.asarray(values), device="cuda")
         k = k.to("cuda").contiguous()
-        v = v.to("cuda", torch.float16).contiguous()
+        v = _lib.to_f16(v)
         groups = self.batch * self.layers * self.heads
         T = k.numel() // (groups * self.d)
         self.tokens = T
@@ -779,6 +892,52 @@ class DenseStore:
     @property
     def cptr(self):
         return ctypes.byref(self.cstruct)
+
+    def meter_dense_stream(self):
+        """Metered dense pass of one (layer, head) (store.py:533-546)."""
+        n = self.tokens
+        pages = (n + self.page_size - 1) // self.page_size
+        self.meter.add_read("header", PAGE_HEADER_BYTES * pages)
+        self.meter.add_read("dense_k_read", n * self.d * VALUE_BYTES_PER_ENTRY)
+        self.meter.add_read("values", n * self.d_v * VALUE_BYTES_PER_ENTRY)
+
+    def logits(self, group, q):
+        """fp32 logits [tokens, G] of one group for q [G, d] (sphkv_dense_store_logits)."""
+        import torch
+
+        l = _lib.require_gpu()
+        q = q.to(device="cuda", dtype=torch.float32).reshape(-1, self.d).contiguous()
+        out = torch.empty((self.tokens, q.shape[0]), dtype=torch.float32, device="cuda")
+        _lib.check(l.sphkv_dense_store_logits(self.cptr, q.data_ptr(), q.shape[0], int(group),
+                                              out.data_ptr(), _lib.stream_ptr()))
+        return out
+
+    def view(self, layer, head, seq=0):
+        """Host (keys, values) of one group in token order, un-swizzled from the
+        pages (bf16 keys and fp16 values as stored, returned as float64)."""
+        import torch
+
+        g = (seq * self.layers + layer) * self.heads + head
+        P, T = self.page_size, self.tokens
+        dp, dvp = (self.d + 15) // 16 * 16, (self.d_v + 15) // 16 * 16
+        npg = self.n_pages_per_group
+
+        def unswz(pool, w, width):
+            blk = pool.view(-1, npg * P, w)[g].view(npg, P, w // 8, 8)
+            i = torch.arange(P, device=blk.device)
+            mask = min(w // 8, 8) - 1
+            chunk = torch.arange(w // 8, device=blk.device)[None, :] ^ (i[:, None] & mask)
+            rows = torch.gather(blk, 2, chunk[None, :, :, None].expand(npg, P, w // 8, 8))
+            return rows.reshape(npg * P, w)[:T, :width].double().cpu().numpy()
+
+        return unswz(self.t_keys, dp, self.d), unswz(self.t_values, dvp, self.d_v)
+
+    def stream_dense(self, layer, head, metered=True):
+        """Metered dense view (store.py:533-546): headers + dense K + values."""
+        keys, values = self.view(layer, head)
+        if metered:
+            self.meter_dense_stream()
+        return keys, values
 
     @property
     def n_pages_per_group(self):

@@ -181,6 +181,43 @@ def test_appends_bit_exact(sk, golden, name):
     check_store_bytes(st, g, p + "app_")
 
 
+@pytest.mark.parametrize("stage", ["pack", "app"])
+@pytest.mark.parametrize("name", CASES)
+def test_sphkv1_import_roundtrip(sk, golden, name, stage, tmp_path):
+    """SPHKV1 import into device pages (store.py:391-427; reference
+    test_store.py:284-305): the reference's own snapshot bytes load, export
+    back byte-identical, keep the size + frag == resident identity, and the
+    loaded pages attend exactly like the packed ones."""
+    g = golden("store")
+    p = name + "_"
+    L, H, T, d, dv, P, G = (int(x) for x in g[p + "dims"])
+    if P % 32:
+        pytest.skip("device pages are multiples of 32 items")
+    tiers = table(sk, g[p + "tiers"])
+    blob = g[p + stage + "_sphkv1"].tobytes()
+    path = tmp_path / "snap.bin"
+    path.write_bytes(blob)
+    st = sk.PagedStore.from_file(str(path), tiers)
+    br = st.resident_breakdown()
+    assert st.to_bytes() == blob
+    assert len(blob) + br.frag_bytes == br.total == int(g[p + stage + "_resident"][-1])
+    st.check_invariants()
+    assert all(np.all(pg.token_ids == -1) for pg in st.pages)
+    ref, *_ = pack_case(sk, g, name)
+    for l in range(L):
+        for h in range(H):
+            a_lg, a_out = sk.decode.attend_heads(ref, l, h, g[p + "q"][l, h])
+            b_lg, b_out = sk.decode.attend_heads(st, l, h, g[p + "q"][l, h])
+            if stage == "pack":
+                assert np.array_equal(a_lg, b_lg) and np.array_equal(a_out, b_out)
+    # appends keep working on an imported store (pools, pointer lists, group_last)
+    st.append_item(0, 0, sk.SphericalKey(0.5, np.full(d - 1, 0.3)), np.ones(dv),
+                   int(tiers.non_drop[0].id))
+    st.check_invariants()
+    with pytest.raises(ValueError):
+        sk.PagedStore.from_bytes(b"NOTSPH" + blob[6:], tiers)
+
+
 # ---------------------------------------------------------------------------
 # attend
 # ---------------------------------------------------------------------------
@@ -254,6 +291,69 @@ def test_split_merge_equals_single_pass(sk):
         again = sk.ada_decode(st, wl.queries, plan)
         assert torch.allclose(one, again, rtol=2e-5, atol=2e-5)
     assert int(plan.ctl.abs().sum()) == 0
+
+
+def _mixed_store(sk, T, G=4, d=64, H=2, seed=3, P=128):
+    import torch
+    from paper_2605_18856_b200 import _lib
+
+    wl = sk.synth.generate(1, 1, H, G, T, d, seed=seed)
+    tiers = table(sk, [(0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8), (3, 12, 14, 8)])
+    st = sk.PagedStore(tiers, 1, H, d, d, P, capacity_tokens=T)
+    n = wl.groups * wl.tokens
+    rng = np.random.default_rng(seed)
+    tier = rng.choice([0, 1, 2, 3], n, p=[0.1, 0.4, 0.4, 0.1]).astype(np.int16)
+    radii = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().sphkv_encode_radii(wl.keys.data_ptr(), _lib.BF16, n, d,
+                                             radii.data_ptr(), _lib.stream_ptr()))
+    sk.pack_device(st, keys=wl.keys.view(-1, d), radii=radii, values=wl.values.view(-1, d),
+                   z=(tier != 0).astype(np.int8), tier=tier, protect=np.zeros(n, np.uint8),
+                   tokens=wl.tokens)
+    return st, wl
+
+
+def test_unit_longer_than_tile_cap(sk, monkeypatch):
+    """A unit with more tiles than the kernel's tile list holds (a direct C-ABI
+    caller's plan) runs as several segments with one online softmax: same
+    outputs as a planner-split plan, logits included."""
+    import torch
+    from paper_2605_18856_b200 import plan as planmod
+
+    st, wl = _mixed_store(sk, 150000)
+    ref = sk.ada_decode(st, wl.queries, sk.plan_store(st, grid=148, units_per_cta=1))
+    cap = planmod.tile_geometry()
+    monkeypatch.setattr(planmod, "tile_geometry", lambda: (cap[0], 1 << 20))
+    big = sk.plan_store(st, groups=[0], grid=1, units_per_cta=1)
+    assert big.n_units == 1 and int(big.group_items[0]) > 2 * 512 * cap[0]
+    got = sk.ada_decode(st, wl.queries, big)
+    assert torch.allclose(ref[:4], got, rtol=2e-5, atol=2e-5)
+    lg = torch.zeros(int(big.group_items.sum()) * 4, dtype=torch.float32, device="cuda")
+    got2 = sk.ada_decode(st, wl.queries, big, logits=lg)
+    assert torch.allclose(ref[:4], got2, rtol=2e-5, atol=2e-5)
+    monkeypatch.undo()
+    want_lg, _ = sk.decode.attend_heads(st, 0, 0, wl.queries[0].double().cpu().numpy())
+    n0 = int(big.group_items[0])
+    assert np.allclose(lg[: n0 * 4].view(n0, 4).T.double().cpu().numpy(), want_lg, rtol=1e-5,
+                       atol=1e-5)
+
+
+def test_dynamic_plan_back_to_back(sk):
+    """Dynamic-queue plans launched back to back on one stream (programmatic
+    dependent launch): no CTA claims from the queue before the previous grid
+    is done, so every launch equals the static plan and the control words
+    end re-armed."""
+    import torch
+
+    st, wl = _mixed_store(sk, 60000, seed=4)
+    ref = sk.ada_decode(st, wl.queries, sk.plan_store(st, grid=148, units_per_cta=1))
+    dyn = sk.plan_store(st, grid=40, units_per_cta=4, dynamic=True)
+    outs = [torch.empty_like(ref) for _ in range(6)]
+    for o in outs:
+        sk.ada_decode(st, wl.queries, dyn, out=o)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.allclose(ref, o, rtol=2e-5, atol=2e-5)
+    assert int(dyn.ctl.abs().sum()) == 0
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
@@ -363,6 +463,79 @@ def test_dense_decode_vs_oracle(sk):
             _, want = O.dense_attend(q[g, gi], keys[g], vals[g])
             err = np.max(np.abs(out[g * 4 + gi] - want)) / np.max(np.abs(want))
             assert err <= 5e-3, err  # bf16 K / q in the dense baseline
+
+
+def test_dense_head_attend_reference_shape(sk):
+    """_head_attend("dense") (decode.py:302-307) returns every logit (one per
+    token, decode.py:63-69 on the stored bf16 keys), the dense output and the
+    reference meter counts (store.py:533-546); view() un-swizzles the pages;
+    dense_logits runs in fp64 on the device."""
+    from paper_2605_18856_b200 import synth
+
+    wl = synth.generate(1, 2, 2, 4, 700, 64, seed=9)
+    ds = sk.DenseStore(2, 2, 64, 64, 256)
+    ds.bulk_load(wl.keys, wl.values)
+    keys = wl.keys.double().cpu().numpy()
+    vals = wl.values.double().cpu().numpy()
+    q = wl.queries.double().cpu().numpy()[1 * 2 + 1, 2]
+    kv, vv = ds.view(1, 1)
+    assert np.array_equal(kv, keys[3]) and np.array_equal(vv, vals[3])
+    ds.meter.reset()
+    lg, out, n, _ = sk.decode._head_attend("dense", ds, 1, 1, q)
+    want_lg, want_out = O.dense_attend(q, keys[3], vals[3])
+    assert n == 700 and lg.shape == (700,)
+    assert np.max(np.abs(lg - want_lg) / np.maximum(1, np.abs(want_lg))) < 1e-5
+    assert np.max(np.abs(out - want_out)) / np.max(np.abs(want_out)) < 5e-3  # bf16 q in the kernel
+    snap = ds.meter.snapshot()
+    assert snap["header"] == 16 * 3 and snap["dense_k_read"] == 700 * 64 * 2
+    assert snap["values"] == 700 * 64 * 2
+    rng = np.random.default_rng(3)
+    kk, qq = rng.standard_normal((333, 48)), rng.standard_normal(48)
+    np.testing.assert_allclose(sk.dense_logits(qq, kk), kk @ qq / math.sqrt(48), rtol=1e-13,
+                               atol=1e-13)
+    with pytest.raises(ValueError):
+        sk.dense_logits(qq, kk[:, :40])
+
+
+def test_angle_head_attend_meters_stream_bytes(sk):
+    """_head_attend("angle") meters header + code + value bytes of every
+    listed page once per call (decode.py:336-342), = expected_stream_bytes."""
+    rng = np.random.default_rng(11)
+    L, H, T, d, P = 1, 2, 900, 64, 256
+    tl = [(0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8), (3, 12, 14, 8)]
+    tiers = sk.TierTable(tuple(sk.TierSpec(*t) for t in tl))
+    r, ang = O.encode_batch(rng.standard_normal((L * H * T, d)))
+    tier = rng.choice([0, 1, 2, 3], (L, H, T)).astype(np.int16)
+    st = sk.pack_pages_arrays(sk.TierAssignment((tier != 0).astype(np.int8), tier,
+                                                np.zeros((L, H, T), bool)),
+                              r.reshape(L, H, T), ang.reshape(L, H, T, d - 1),
+                              rng.standard_normal((L, H, T, d)), tiers, P)
+    st.meter.reset()
+    sk.decode._head_attend("angle", st, 0, 1, rng.standard_normal(d))
+    snap = st.meter.snapshot()
+    assert snap["header"] + snap["k_codes"] + snap["values"] == st.expected_stream_bytes(0, 1)
+    assert snap["dense_k_read"] == snap["dense_k_write"] == 0
+
+
+def test_pack_values_single_rounding(sk):
+    """Values are rounded to fp16 once, as numpy astype(np.float16) does
+    (store.py:383), for float64 host arrays and float64 device tensors."""
+    import torch
+
+    rng = np.random.default_rng(2)
+    L, H, T, d, P = 1, 1, 2048, 64, 256
+    tl = [(0, 0, 0, 0), (1, 4, 8, 8)]
+    tiers = sk.TierTable(tuple(sk.TierSpec(*t) for t in tl))
+    r, ang = O.encode_batch(rng.standard_normal((T, d)))
+    vals = rng.standard_normal((L, H, T, d))
+    asg = sk.TierAssignment(np.ones((L, H, T), np.int8), np.ones((L, H, T), np.int16),
+                            np.zeros((L, H, T), bool))
+    st = sk.pack_pages_arrays(asg, r.reshape(L, H, T), ang.reshape(L, H, T, d - 1), vals, tiers, P)
+    got = np.concatenate([p.values for p in st.pages])
+    want = vals.reshape(T, d).astype(np.float16).astype(np.float64)
+    assert np.array_equal(got, want)
+    out = sk._lib.to_f16(torch.as_tensor(vals.reshape(-1), device="cuda"))
+    assert np.array_equal(out.cpu().numpy(), vals.reshape(-1).astype(np.float16))
 
 
 # ---------------------------------------------------------------------------
