@@ -41,6 +41,17 @@ constexpr double kPi = 3.141592653589793;      // math.pi
 constexpr double kNormEps = 1e-12;             // codec.py:218
 constexpr int SM_COUNT = 148;
 
+// A tier table passed BY VALUE as a kernel parameter (512 bytes): no device
+// copy, hence no hidden allocation and capture-safe in CUDA graphs.
+struct TierSet {
+  sphkv_tier_t t[SPHKV_MAX_TIERS];
+};
+inline TierSet make_tierset(const sphkv_tier_t* host, int n) {
+  TierSet ts{};
+  for (int i = 0; i < n && i < SPHKV_MAX_TIERS; ++i) ts.t[i] = host[i];
+  return ts;
+}
+
 __host__ __device__ inline int64_t div_up(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Device angle-code layout of a page: "word-interleaved, item-major" (WI).

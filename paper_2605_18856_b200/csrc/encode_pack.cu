@@ -556,7 +556,7 @@ __global__ void k_append_write(sphkv_store_t st, int n, const int16_t* __restric
 // score_and_best_tier per appended state (controller.py:163-198)
 __global__ void k_score_append(const double* __restrict__ radii, int groups_per_seq, int heads,
                                const double* __restrict__ u_hat, const double* __restrict__ s_hat,
-                               double r_q, double om, double at, double ar, sphkv_tier_t* tiers,
+                               double r_q, double om, double at, double ar, const TierSet ts,
                                int NT, double lam, int d, int64_t n, int16_t* tier_out,
                                double* score_out, double* nu_out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -570,9 +570,9 @@ __global__ void k_score_append(const double* __restrict__ radii, int groups_per_
   int best = -1;
   double best_s = -INFINITY;
   for (int t = 0; t < NT; ++t) {
-    double et = t == 0 ? 1.0 : tiers[t].eps_theta, er = t == 0 ? 1.0 : tiers[t].eps_r;
+    double et = t == 0 ? 1.0 : ts.t[t].eps_theta, er = t == 0 ? 1.0 : ts.t[t].eps_r;
     double dist = __dadd_rn(__dmul_rn(w_theta, et), __dmul_rn(w_r, er));
-    int rate = t == 0 ? 0 : (d - 1) * tiers[t].angle_bits + tiers[t].radius_bits + tiers[t].meta_bits;
+    int rate = t == 0 ? 0 : (d - 1) * ts.t[t].angle_bits + ts.t[t].radius_bits + ts.t[t].meta_bits;
     double s = __dadd_rn(-dist, -__dmul_rn(lam, (double)rate));
     if (s > best_s) {
       best_s = s;
@@ -580,12 +580,12 @@ __global__ void k_score_append(const double* __restrict__ radii, int groups_per_
     }
   }
   double d_drop = __dadd_rn(w_theta, w_r);
-  double et = best == 0 ? 1.0 : tiers[best].eps_theta, er = best == 0 ? 1.0 : tiers[best].eps_r;
+  double et = best == 0 ? 1.0 : ts.t[best].eps_theta, er = best == 0 ? 1.0 : ts.t[best].eps_r;
   double d_best = __dadd_rn(__dmul_rn(w_theta, et), __dmul_rn(w_r, er));
   int rate = best == 0 ? 0
-                       : (d - 1) * tiers[best].angle_bits + tiers[best].radius_bits +
-                             tiers[best].meta_bits;
-  tier_out[i] = (int16_t)tiers[best].id;
+                       : (d - 1) * ts.t[best].angle_bits + ts.t[best].radius_bits +
+                             ts.t[best].meta_bits;
+  tier_out[i] = (int16_t)ts.t[best].id;
   if (score_out) score_out[i] = best_s;
   if (nu_out) nu_out[i] = __ddiv_rn(__dadd_rn(d_drop, -d_best), __dadd_rn((double)rate, 1e-12));
 }
@@ -954,16 +954,12 @@ extern "C" int sphkv_score_append(const double* radii, int groups_per_seq, int h
   (void)heads;
   if (n_tiers < 2 || n_tiers > SPHKV_MAX_TIERS) return fail(SPHKV_E_VALUE, "bad tier count");
   if (n == 0) return SPHKV_OK;
-  sphkv_tier_t* dt = nullptr;
-  SPHKV_CUDA_TRY(cudaMallocAsync((void**)&dt, sizeof(sphkv_tier_t) * n_tiers, stream));
-  SPHKV_CUDA_TRY(cudaMemcpyAsync(dt, tiers_host, sizeof(sphkv_tier_t) * n_tiers,
-                                 cudaMemcpyHostToDevice, stream));
   k_score_append<<<(int)div_up(n, 128), 128, 0, stream>>>(radii, groups_per_seq, heads, u_hat,
                                                           s_hat, r_q, omega, alpha_theta, alpha_r,
-                                                          dt, n_tiers, lam, d, n, tier_out,
-                                                          score_out, nu_out);
+                                                          make_tierset(tiers_host, n_tiers),
+                                                          n_tiers, lam, d, n, tier_out, score_out,
+                                                          nu_out);
   SPHKV_LAUNCH_CHECK();
-  SPHKV_CUDA_TRY(cudaFreeAsync(dt, stream));
   return SPHKV_OK;
 }
 

@@ -21,7 +21,7 @@ namespace sphkv {
 
 __global__ void k_rdr_score(const double* __restrict__ radii, const double* __restrict__ u_hat,
                             const double* __restrict__ s_hat, const double* __restrict__ seg_omega,
-                            double r_q, double at, double ar, sphkv_tier_t tiers_arr[SPHKV_MAX_TIERS],
+                            double r_q, double at, double ar, const TierSet tiers_arr,
                             int NT, double lam, const uint8_t* __restrict__ protect, int LH, int T,
                             int d, int16_t* best_tier, double* score, double* nu, double* d_drop_out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -39,7 +39,7 @@ __global__ void k_rdr_score(const double* __restrict__ radii, const double* __re
   int best = 0;
   double bs = protect[i] ? -INFINITY : -dd;
   for (int t = 1; t < NT; ++t) {
-    const sphkv_tier_t tt = tiers_arr[t];
+    const sphkv_tier_t tt = tiers_arr.t[t];
     const int rate = (d - 1) * tt.angle_bits + tt.radius_bits + tt.meta_bits;
     double s = __dadd_rn(-__dadd_rn(__dmul_rn(w_theta, tt.eps_theta), __dmul_rn(w_r, tt.eps_r)),
                          -__dmul_rn(lam, (double)rate));
@@ -53,11 +53,11 @@ __global__ void k_rdr_score(const double* __restrict__ radii, const double* __re
     db = __dadd_rn(__dmul_rn(w_theta, 1.0), __dmul_rn(w_r, 1.0));
     rb = 0.0;
   } else {
-    const sphkv_tier_t tt = tiers_arr[best];
+    const sphkv_tier_t tt = tiers_arr.t[best];
     db = __dadd_rn(__dmul_rn(w_theta, tt.eps_theta), __dmul_rn(w_r, tt.eps_r));
     rb = (double)((d - 1) * tt.angle_bits + tt.radius_bits + tt.meta_bits);
   }
-  best_tier[i] = (int16_t)tiers_arr[best].id;
+  best_tier[i] = (int16_t)tiers_arr.t[best].id;
   if (score) score[i] = bs;
   if (nu) nu[i] = __ddiv_rn(__dadd_rn(dd, -db), __dadd_rn(rb, 1e-12));
   if (d_drop_out) d_drop_out[i] = dd;
@@ -112,12 +112,71 @@ __global__ void k_costs(const int64_t* __restrict__ sidx, const int16_t* __restr
   cost[i] = protect[s] ? 0 : rate_of(tr, best[s]);
 }
 
+// Device-resident state of the greedy rounds (no host round trips): the
+// scan position p, the remaining budget R, the cost cap and the first
+// rejected sorted position of the current round.
+struct GreedyState {
+  long long p, R;
+  int cap, finished;
+  unsigned long long first;
+};
+
+__global__ void k_greedy_init(GreedyState* gs, const unsigned long long* n_prot, long long budget,
+                              long long max_rate, int* status) {
+  const long long R = budget - (long long)*n_prot * max_rate;
+  gs->p = 0;
+  gs->R = R;
+  gs->cap = 0x7fffffff;
+  gs->finished = R < 0;
+  gs->first = ~0ull;
+  *status = R < 0 ? 1 : 0;  // 1: infeasible protection (controller.py:316-322)
+}
+
 __global__ void k_masked(const int32_t* __restrict__ cost, const uint8_t* __restrict__ done,
-                         int64_t n, int64_t p, int32_t cap, int64_t* out) {
+                         int64_t n, const GreedyState* __restrict__ gs, int64_t* out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int32_t c = cost[i];
-  out[i] = (i >= p && !done[i] && c > 0 && c < cap) ? (int64_t)c : 0;
+  const int32_t c = cost[i];
+  out[i] = (!gs->finished && i >= gs->p && !done[i] && c > 0 && c < gs->cap) ? (int64_t)c : 0;
+}
+
+// masked[i] = 0 below p, so scan[i] is the cost taken since p
+__global__ void k_first_over_gs(const int64_t* __restrict__ scan, const int64_t* __restrict__ masked,
+                                int64_t n, GreedyState* gs) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || gs->finished || i < gs->p) return;
+  if (masked[i] > 0 && scan[i] > gs->R) atomicMin(&gs->first, (unsigned long long)i);
+}
+
+__global__ void k_accept_gs(const int64_t* __restrict__ sidx, const int16_t* __restrict__ best,
+                            const int64_t* __restrict__ masked, int64_t n,
+                            const GreedyState* __restrict__ gs, uint8_t* done, int8_t* z,
+                            int16_t* tier) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n || gs->finished || i < gs->p || (unsigned long long)i >= gs->first) return;
+  if (masked[i] > 0) {
+    int64_t s = sidx[i];
+    z[s] = 1;
+    tier[s] = best[s];
+    done[i] = 1;
+  }
+}
+
+// end of a round: the first rejected item shrinks the budget and the cap
+__global__ void k_greedy_update(const int64_t* __restrict__ scan, const int32_t* __restrict__ cost,
+                                int64_t n, GreedyState* gs) {
+  if (gs->finished) return;
+  const unsigned long long first = gs->first;
+  if (first == ~0ull) {
+    gs->finished = 1;
+    return;
+  }
+  const int64_t hi = (int64_t)first;
+  gs->R -= hi > 0 ? scan[hi - 1] : 0;
+  gs->cap = min(gs->cap, cost[hi]);
+  gs->p = hi + 1;
+  gs->first = ~0ull;
+  if (gs->p >= n) gs->finished = 1;
 }
 
 __global__ void k_first_over(const int64_t* __restrict__ scan, const int64_t* __restrict__ masked,
@@ -211,16 +270,12 @@ extern "C" int sphkv_rdr_score(const double* radii, const double* u_hat, const d
   if (d < 2) return fail(SPHKV_E_VALUE, "head dimension must be >= 2");
   int64_t n = (int64_t)layers * heads * tokens;
   if (n == 0) return SPHKV_OK;
-  sphkv_tier_t* dt = nullptr;
-  SPHKV_CUDA_TRY(cudaMallocAsync((void**)&dt, sizeof(sphkv_tier_t) * SPHKV_MAX_TIERS, stream));
-  SPHKV_CUDA_TRY(cudaMemcpyAsync(dt, tiers_host, sizeof(sphkv_tier_t) * n_tiers,
-                                 cudaMemcpyHostToDevice, stream));
   k_rdr_score<<<(int)div_up(n, 256), 256, 0, stream>>>(radii, u_hat, s_hat, seg_omega, r_q,
-                                                       alpha_theta, alpha_r, dt, n_tiers, lam,
-                                                       protect, layers * heads, tokens, d,
+                                                       alpha_theta, alpha_r,
+                                                       make_tierset(tiers_host, n_tiers), n_tiers,
+                                                       lam, protect, layers * heads, tokens, d,
                                                        best_tier, score, nu, d_drop);
   SPHKV_LAUNCH_CHECK();
-  SPHKV_CUDA_TRY(cudaFreeAsync(dt, stream));
   return SPHKV_OK;
 }
 
@@ -298,17 +353,15 @@ extern "C" int sphkv_rdr_allocate_greedy(const int16_t* best_tier, const double*
   const int64_t max_rate = tr.rate[n_tiers - 1];
   RdrWs w = carve(workspace, n);
   const int nb = (int)div_up(n, 256);
-  // protected demand (controller.py:316-322)
+  // protected demand (controller.py:316-322) and the round state, on the device
+  GreedyState* gs = reinterpret_cast<GreedyState*>(w.scal + 2);
+  int* status = reinterpret_cast<int*>(w.scal + 7);
   SPHKV_CUDA_TRY(cudaMemsetAsync(w.scal, 0, 64, stream));
   k_count_protect<<<4 * SM_COUNT, 256, 0, stream>>>(protect, n, w.scal + 1);
   SPHKV_LAUNCH_CHECK();
-  unsigned long long n_prot = 0;
-  SPHKV_CUDA_TRY(cudaMemcpyAsync(&n_prot, w.scal + 1, 8, cudaMemcpyDeviceToHost, stream));
-  SPHKV_CUDA_TRY(cudaStreamSynchronize(stream));
-  int64_t R = budget_bits - (int64_t)n_prot * max_rate;
-  if (R < 0)
-    return fail(SPHKV_E_INFEASIBLE, "protected demand %lld bits exceeds budget %lld",
-                (long long)n_prot * max_rate, (long long)budget_bits);
+  k_greedy_init<<<1, 1, 0, stream>>>(gs, w.scal + 1, (long long)budget_bits, (long long)max_rate,
+                                     status);
+  SPHKV_LAUNCH_CHECK();
   k_init_assign<<<nb, 256, 0, stream>>>(best_tier, protect, n, max_id, 0, z, tier);
   SPHKV_LAUNCH_CHECK();
   int64_t* sidx = nullptr;
@@ -316,44 +369,31 @@ extern "C" int sphkv_rdr_allocate_greedy(const int16_t* best_tier, const double*
   k_costs<<<nb, 256, 0, stream>>>(sidx, best_tier, protect, n, tr, w.cost);
   SPHKV_LAUNCH_CHECK();
   SPHKV_CUDA_TRY(cudaMemsetAsync(w.done, 0, n, stream));
-  int64_t p = 0;
-  int32_t cap = 0x7fffffff;
-  for (int round = 0; round <= SPHKV_MAX_TIERS + 1; ++round) {
-    k_masked<<<nb, 256, 0, stream>>>(w.cost, w.done, n, p, cap, w.masked);
+  // Every round rejects one item whose cost is below the cap, so the cap
+  // strictly decreases: at most (distinct non-drop rates) + 1 rounds.  They
+  // are all enqueued; finished rounds are no-ops on the device.
+  for (int round = 0; round < n_tiers + 1; ++round) {
+    k_masked<<<nb, 256, 0, stream>>>(w.cost, w.done, n, gs, w.masked);
     SPHKV_LAUNCH_CHECK();
     size_t tb = w.cub_bytes;
     SPHKV_CUDA_TRY(cub::DeviceScan::InclusiveSum(w.cub, tb, w.masked, w.scan, (int)n, stream));
-    SPHKV_CUDA_TRY(cudaMemsetAsync(w.scal, 0xff, 8, stream));
-    // prefix sum relative to position p: subtract scan[p-1]
-    int64_t before = 0;
-    if (p > 0) {
-      SPHKV_CUDA_TRY(cudaMemcpyAsync(&before, w.scan + p - 1, 8, cudaMemcpyDeviceToHost, stream));
-      SPHKV_CUDA_TRY(cudaStreamSynchronize(stream));
-    }
-    k_first_over<<<nb, 256, 0, stream>>>(w.scan, w.masked, n, p, R + before, w.scal);
+    k_first_over_gs<<<nb, 256, 0, stream>>>(w.scan, w.masked, n, gs);
     SPHKV_LAUNCH_CHECK();
-    unsigned long long first = 0;
-    SPHKV_CUDA_TRY(cudaMemcpyAsync(&first, w.scal, 8, cudaMemcpyDeviceToHost, stream));
-    SPHKV_CUDA_TRY(cudaStreamSynchronize(stream));
-    int64_t hi = (first == ~0ull) ? n : (int64_t)first;
-    if (hi > p) {
-      k_accept<<<(int)div_up(hi - p, 256), 256, 0, stream>>>(sidx, best_tier, w.masked, p, hi,
-                                                             w.done, z, tier);
-      SPHKV_LAUNCH_CHECK();
-    }
-    if (first == ~0ull) return SPHKV_OK;
-    // item `first` is rejected: remaining budget and the cost cap shrink
-    int64_t upto = 0;
-    int32_t cfirst = 0;
-    if (hi > 0) SPHKV_CUDA_TRY(cudaMemcpyAsync(&upto, w.scan + hi - 1, 8, cudaMemcpyDeviceToHost, stream));
-    SPHKV_CUDA_TRY(cudaMemcpyAsync(&cfirst, w.cost + hi, 4, cudaMemcpyDeviceToHost, stream));
-    SPHKV_CUDA_TRY(cudaStreamSynchronize(stream));
-    R -= (upto - before);
-    cap = cfirst < cap ? cfirst : cap;
-    p = hi + 1;
-    if (p >= n) return SPHKV_OK;
+    k_accept_gs<<<nb, 256, 0, stream>>>(sidx, best_tier, w.masked, n, gs, w.done, z, tier);
+    SPHKV_LAUNCH_CHECK();
+    k_greedy_update<<<1, 1, 0, stream>>>(w.scan, w.cost, n, gs);
+    SPHKV_LAUNCH_CHECK();
   }
-  return fail(SPHKV_E_CUDA, "greedy allocation did not converge");
+  // one host read at the end: the infeasibility status and convergence
+  int host[2] = {0, 0};
+  SPHKV_CUDA_TRY(cudaMemcpyAsync(&host[0], status, 4, cudaMemcpyDeviceToHost, stream));
+  SPHKV_CUDA_TRY(cudaMemcpyAsync(&host[1], &gs->finished, 4, cudaMemcpyDeviceToHost, stream));
+  SPHKV_CUDA_TRY(cudaStreamSynchronize(stream));
+  if (host[0] == 1)
+    return fail(SPHKV_E_INFEASIBLE, "protected demand exceeds budget %lld bits",
+                (long long)budget_bits);
+  if (!host[1]) return fail(SPHKV_E_CUDA, "greedy allocation did not converge");
+  return SPHKV_OK;
 }
 
 extern "C" int sphkv_rdr_downtier(const int16_t* best_tier, const double* nu,
