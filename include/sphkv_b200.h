@@ -207,6 +207,16 @@ int sphkv_pack_pages(const sphkv_store_t* st, const void* keys, int key_dtype,
                      const uint16_t* values, const int8_t* z, const int16_t* tier,
                      const uint8_t* protect, int tokens, void* workspace,
                      int64_t workspace_bytes, cudaStream_t stream);
+/* Same, for the contiguous groups [group0, group0 + n_groups) only: every
+ * input array is relative to group0 ([n_groups * tokens] states).  Packs one
+ * sequence (or one shard) at a time into a shared store, so the raw K/V of
+ * only that part needs to be resident; pages append after the existing ones
+ * and pointer lists of other groups are untouched. */
+int sphkv_pack_pages_groups(const sphkv_store_t* st, int group0, int n_groups, const void* keys,
+                            int key_dtype, const double* angles, const double* radii,
+                            const uint16_t* values, const int8_t* z, const int16_t* tier,
+                            const uint8_t* protect, int tokens, void* workspace,
+                            int64_t workspace_bytes, cudaStream_t stream);
 int64_t sphkv_pack_workspace_bytes(int batch, int layers, int heads, int tokens);
 
 /* PagedStore.append_item for one new state per group (decode.py:454-498):
@@ -232,6 +242,12 @@ int sphkv_score_append(const double* radii, int groups_per_seq, int heads,
  * [groups*T, d] (dtype), values fp16 [groups*T, d_v] -> swizzled pages. */
 int sphkv_dense_fill(const sphkv_dense_store_t* st, const void* keys, int key_dtype,
                      const uint16_t* values, cudaStream_t stream);
+
+/* Same for the contiguous groups [group0, group0 + n_groups) (inputs relative
+ * to group0): fills one sequence / shard of a batched dense store. */
+int sphkv_dense_fill_groups(const sphkv_dense_store_t* st, int group0, int n_groups,
+                            const void* keys, int key_dtype, const uint16_t* values,
+                            cudaStream_t stream);
 
 /* fp64 -> fp16 with one round-to-nearest-even (numpy astype(np.float16),
  * the SPHKV1 value type, store.py:383); torch's double->half conversion
@@ -306,6 +322,14 @@ int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const float* q, int 
                              const int32_t* slot_group, const int32_t* slot_begin,
                              int n_groups, int32_t* ctl, float* out, int dynamic, int grid,
                              cudaStream_t stream);
+
+/* Fused dense decode restricted to tokens >= token_begin of every planned
+ * group (a sliding-window layer: the window's last W tokens only). */
+int sphkv_dense_decode_window(const sphkv_dense_store_t* st, const float* q, int G,
+                              const sphkv_unit_t* units, int n_units, float* partials,
+                              const int32_t* slot_group, const int32_t* slot_begin, int n_groups,
+                              int32_t* ctl, float* out, int dynamic, int token_begin, int grid,
+                              cudaStream_t stream);
 
 /* Reconstruct-then-dot negative control (decode.py:195-217):
  * decode the codes of pages[i] (pointer order) into dense key rows

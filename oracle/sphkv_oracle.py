@@ -548,3 +548,134 @@ def lse_merge(m, lsum, acc):
     A = (wgt[..., None] * acc).sum(axis=0)
     out = np.where(L[..., None] > 0, A / np.where(L > 0, L, 1.0)[..., None], 0.0)
     return out
+
+
+# ---------------------------------------------------------------------------
+# host-only workload pieces for bench.py's reference arm (no product code):
+# one (layer, kv-head) slice generated, calibrated, scored, allocated and
+# packed entirely here, in numpy
+# ---------------------------------------------------------------------------
+
+PREFIX_FRAC = 2944 / 4096     # pkg/configs/panel.cfg:8
+RETRIEVED_FRAC = 3584 / 4096  # pkg/configs/panel.cfg:9
+
+
+def segments_for(T):
+    seg = np.full(T, 2, dtype=np.int8)
+    seg[: int(round(T * PREFIX_FRAC))] = 0
+    seg[int(round(T * PREFIX_FRAC)): int(round(T * RETRIEVED_FRAC))] = 1
+    return seg
+
+
+def generate_slice(T, d, G, seed, outlier_frac=0.01, outlier_mult=4.0, query_gain=4.0):
+    """One (layer, kv-head) slice of the reference workload distribution
+    (workload.py:204-248): unit topic; prefix tokens -topic + 0.35 N/sqrt(d),
+    radius |N(1.6, 0.15)|; retrieved/recent topic + 0.6 N/sqrt(d), radius
+    |N(1.0, 0.2)|; 1% outliers x4; values N(0, 1); G queries topic + 0.5
+    N/sqrt(d) with norm 4 sqrt(d) |N(1, 0.05)|.  Keys are rounded to bf16 and
+    values to fp16 as the benchmark stores them.  Returns (keys, values, q,
+    prefill-row queries for the features, segments)."""
+    rng = np.random.default_rng(seed)
+    topic = rng.standard_normal(d)
+    topic /= np.linalg.norm(topic)
+    seg = segments_for(T)
+    pre = (seg == 0)[:, None]
+    g = rng.standard_normal((T, d)) / np.sqrt(d)
+    base = np.where(pre, -topic + 0.35 * g, topic + 0.6 * g)
+    base /= np.linalg.norm(base, axis=-1, keepdims=True)
+    radii = np.where(pre[:, 0], np.abs(rng.normal(1.6, 0.15, T)), np.abs(rng.normal(1.0, 0.2, T)))
+    radii = np.where(rng.random(T) < outlier_frac, radii * outlier_mult, radii)
+    keys = _bf16(base * radii[:, None])
+    values = rng.standard_normal((T, d)).astype(np.float16).astype(np.float64)
+
+    def qdraw(n):
+        qd = topic + 0.5 * rng.standard_normal((n, d)) / np.sqrt(d)
+        qd /= np.linalg.norm(qd, axis=-1, keepdims=True)
+        return qd * (query_gain * np.sqrt(d) * np.abs(rng.normal(1.0, 0.05, (n, 1))))
+
+    q = qdraw(G).astype(np.float32).astype(np.float64)
+    return keys, values, q, qdraw, seg
+
+
+def _bf16(x):
+    """Round fp64 -> bf16 (nearest-even via fp32) -> fp64, as the benchmark stores keys."""
+    f = np.asarray(x, dtype=np.float32)
+    b = f.view(np.uint32).astype(np.uint64)
+    b = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16
+    return b.astype(np.uint32).view(np.float32).astype(np.float64)
+
+
+def features_slice(keys, qdraw, rows=512, seed=1):
+    """controller.compute_features (controller.py:99-142) for one slice: a
+    causal softmax over <= `rows` sampled prefill rows.  With a single head the
+    per-(l, h) normalization gives u_hat = 1 and s_hat = 0 (stated in the
+    reference arm's sample description).  Returns (u_raw, inv_margin, r_q)."""
+    T, d = keys.shape
+    window = max(T // 8, 1)
+    idx = np.unique(np.round(np.linspace(0, T - 1, min(rows, T))).astype(int))
+    q = qdraw(len(idx))
+    logits = q @ keys.T / math.sqrt(d)
+    mask = np.arange(T)[None, :] > idx[:, None]
+    logits = np.where(mask, -np.inf, logits)
+    z = logits - logits.max(axis=1, keepdims=True)
+    w = np.exp(z)
+    w /= w.sum(axis=1, keepdims=True)
+    old = np.arange(T)[None, :] <= (idx[:, None] - window)
+    u_raw = float(np.mean(np.sum(np.where(old, w, 0.0), axis=1)))
+    ok = idx >= 1
+    top2 = np.partition(logits[ok], -2, axis=1)[:, -2:]
+    inv_m = float(np.mean(1.0 / (top2[:, 1] - top2[:, 0] + 1e-6)))
+    return u_raw, inv_m, float(np.mean(np.linalg.norm(q, axis=-1)))
+
+
+def calibrate(tiers, sample_keys, seed):
+    """TierTable.calibrate / calibrate_distortion (codec.py:172-176, 485-522):
+    eps_theta = RMS difference of the angular recurrence on exact vs coded
+    key angles against seeded random query directions; eps_r = RMS radius
+    decode error over the sample's max-radius scale.  Returns {id: (eps_t, eps_r)}."""
+    r, k_ang = encode_batch(np.asarray(sample_keys, dtype=np.float64))
+    out = {}
+    for t in tiers:
+        if t[0] == 0:
+            continue
+        rng = np.random.default_rng(seed)
+        n, d = k_ang.shape[0], k_ang.shape[1] + 1
+        k_dec = dequantize_angles(quantize_angles(k_ang, t[1]), t[1])
+        q = rng.standard_normal((n, d))
+        q /= np.linalg.norm(q, axis=1, keepdims=True) + NORM_EPS
+        qa = angles_from_unit(q)
+
+        def paired(qa_, ka):
+            cq, sq = np.cos(qa_), np.sin(qa_)
+            ck, sk = np.cos(ka), np.sin(ka)
+            prods = np.cumprod(sq * sk, axis=1)
+            acc = cq[:, 0] * ck[:, 0]
+            acc = acc + np.sum(prods[:, :-1] * cq[:, 1:] * ck[:, 1:], axis=1)
+            return acc + prods[:, -1]
+
+        eps_t = math.sqrt(float(np.sum((paired(qa, k_ang) - paired(qa, k_dec)) ** 2)) / n)
+        scale = float(r.max()) + NORM_EPS
+        levels = float((1 << t[2]) - 1)
+        codes = np.array([int(round(min(max(x / scale, 0.0), 1.0) * levels)) for x in r])
+        eps_r = math.sqrt(float(np.mean(((codes / levels * scale - r) / scale) ** 2)))
+        out[t[0]] = (eps_t, eps_r)
+    return out
+
+
+def resident_total(z, tier, tiers, d, d_v, P):
+    """Resident bytes (store.py:178-203, 326-336) of one (l, h) slice's pages."""
+    total, n_pages = 0, 0
+    for t in tiers:
+        if t[0] == 0:
+            continue
+        c = int(np.count_nonzero((z == 1) & (tier == t[0])))
+        full, rem = c // P, c % P
+
+        def page_bytes(n):
+            return (packed_nbytes(n * (d - 1), t[1]) + packed_nbytes(n, t[2]) + n * d_v * 2
+                    + (n * t[3] + 7) // 8 + (n + 7) // 8)
+
+        slot = ((d - 1) * t[1] + t[2] + t[3] + 7) // 8 + d_v * 2
+        total += full * page_bytes(P) + (page_bytes(rem) + (P - rem) * slot if rem else 0)
+        n_pages += full + (1 if rem else 0)
+    return total + PAGE_HEADER_BYTES * n_pages + FILE_DIRECTORY_BYTES + PTR_ENTRY_BYTES * (1 + n_pages)

@@ -88,6 +88,8 @@ def _declare(lib):
         "sphkv_store_build_lut": (c_int, [vp, vp]),
         "sphkv_pack_pages": (c_int, [vp, vp, i, vp, vp, vp, vp, vp, vp, i, vp, i64, vp]),
         "sphkv_pack_workspace_bytes": (c_int64, [i, i, i, i]),
+        "sphkv_pack_pages_groups": (c_int, [vp, i, i, vp, i, vp, vp, vp, vp, vp, vp, i, vp, i64,
+                                            vp]),
         "sphkv_append": (c_int, [vp, vp, i, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
         "sphkv_append_workspace_bytes": (c_int64, [i]),
         "sphkv_score_append": (c_int, [vp, i, i, vp, vp, d, d, d, d, vp, i, d, i, i64,
@@ -95,6 +97,7 @@ def _declare(lib):
         "sphkv_export_streams": (c_int, [vp, i, vp, vp, vp]),
         "sphkv_import_streams": (c_int, [vp, i, vp, vp, vp]),
         "sphkv_dense_fill": (c_int, [vp, vp, i, vp, vp]),
+        "sphkv_dense_fill_groups": (c_int, [vp, i, i, vp, i, vp, vp]),
         "sphkv_ada_decode": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp]),
         "sphkv_dense_decode": (c_int, [vp, vp, i, vp, i, vp, i, vp]),
         "sphkv_lse_merge": (c_int, [vp, vp, i, i, i, vp, vp]),
@@ -104,6 +107,8 @@ def _declare(lib):
                                              i, vp]),
         "sphkv_ada_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
         "sphkv_dense_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
+        "sphkv_dense_decode_window": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, i,
+                                              vp]),
         "sphkv_partial_floats": (c_int64, [i, i]),
         "sphkv_f64_to_f16": (c_int, [vp, i64, vp, vp]),
         "sphkv_recon_dot": (c_int, [vp, i, i64, i, vp, i, vp, vp]),

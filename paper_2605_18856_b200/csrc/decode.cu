@@ -752,6 +752,7 @@ struct DenseParams {
   int n_units;
   float* partials;
   int dp, dvp;            // padded key / value widths
+  int tok_lo;             // first attended token (sliding window); 0 = all
   uint32_t smem_k, smem_v, smem_p, smem_bar;
   int pslot_bytes, prow_bytes;
   FusedCtl fz;
@@ -790,7 +791,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
   uint32_t gbase = 0;
   for (int u = fused_first_unit(p.fz, &s_next); u < p.n_units;) {
     const sphkv_unit_t unit = p.units[u];
-    const int t_begin = unit.ptr_begin * tiles_per_page;
+    const int t_begin = max(unit.ptr_begin * tiles_per_page, p.tok_lo / DN_TI);
     int t_end = unit.ptr_end * tiles_per_page;
     const int t_max = (st.tokens + DN_TI - 1) / DN_TI;
     if (t_end > t_max) t_end = t_max;
@@ -852,8 +853,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
 #pragma unroll
           for (int mi = 0; mi < DN_TI / 16; ++mi) {
             int i0 = mi * 16 + (lane >> 2);
-            if (tok0 + i0 < st.tokens) m = fmaxf(m, c[mi][h]);
-            if (tok0 + i0 + 8 < st.tokens) m = fmaxf(m, c[mi][2 + h]);
+            if (tok0 + i0 < st.tokens && tok0 + i0 >= p.tok_lo) m = fmaxf(m, c[mi][h]);
+            if (tok0 + i0 + 8 < st.tokens && tok0 + i0 + 8 >= p.tok_lo) m = fmaxf(m, c[mi][2 + h]);
           }
           m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
           m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
@@ -864,7 +865,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
 #pragma unroll
             for (int rr = 0; rr < 2; ++rr) {
               int i0 = mi * 16 + (lane >> 2) + rr * 8;
-              float e = (tok0 + i0 < st.tokens) ? exp2f(c[mi][2 * rr + h] - m) : 0.f;
+              float e = (tok0 + i0 < st.tokens && tok0 + i0 >= p.tok_lo)
+                            ? exp2f(c[mi][2 * rr + h] - m) : 0.f;
               __half hv = __float2half_rn(e);
               s += __half2float(hv);
               if (g < p.G) *reinterpret_cast<__half*>(slot + g * p.prow_bytes + i0 * 2) = hv;
@@ -1124,7 +1126,7 @@ static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
 
 static int dense_decode_impl(const sphkv_dense_store_t* st, const float* q, int G,
                              const sphkv_unit_t* units, int n_units, float* partials, int grid,
-                             const FusedCtl& fz, cudaStream_t stream) {
+                             const FusedCtl& fz, cudaStream_t stream, int tok_lo = 0) {
   if (!st || !q || !units || !partials) return fail(SPHKV_E_VALUE, "null argument");
   if (G < 1 || G > 8) return fail(SPHKV_E_UNSUPPORTED, "GQA group size %d outside [1, 8]", G);
   if (st->d > 128 || st->d_v > 128) return fail(SPHKV_E_UNSUPPORTED, "d/d_v above 128");
@@ -1141,6 +1143,8 @@ static int dense_decode_impl(const sphkv_dense_store_t* st, const float* q, int 
   p.fz = fz;
   p.dp = (st->d + 15) / 16 * 16;
   p.dvp = (st->d_v + 15) / 16 * 16;
+  if (tok_lo < 0 || tok_lo > st->tokens) return fail(SPHKV_E_VALUE, "token_begin %d", tok_lo);
+  p.tok_lo = tok_lo;
   p.prow_bytes = DN_TI * 2 + PROW_PAD;
   p.pslot_bytes = (int)align_up(8 * p.prow_bytes + 64, 128);
   size_t off = 0;
@@ -1233,6 +1237,17 @@ extern "C" int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const flo
   int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
   if (rc) return rc;
   return dense_decode_impl(st, q, G, units, n_units, partials, grid, f, stream);
+}
+
+extern "C" int sphkv_dense_decode_window(const sphkv_dense_store_t* st, const float* q, int G,
+                                         const sphkv_unit_t* units, int n_units, float* partials,
+                                         const int32_t* slot_group, const int32_t* slot_begin,
+                                         int n_groups, int32_t* ctl, float* out, int dynamic,
+                                         int token_begin, int grid, cudaStream_t stream) {
+  FusedCtl f;
+  int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
+  if (rc) return rc;
+  return dense_decode_impl(st, q, G, units, n_units, partials, grid, f, stream, token_begin);
 }
 
 // Debug builds (-DSPHKV_DBG_TIMING) only: per-CTA (start, end) globaltimer of

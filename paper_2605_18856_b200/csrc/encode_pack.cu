@@ -109,14 +109,15 @@ __global__ void k_store_reset(sphkv_store_t st) {
 }
 
 // per group, per tier-index retained counts
-__global__ void k_pack_count(sphkv_store_t st, int T, const int8_t* __restrict__ z,
+// (block = group g0 + blockIdx.x; input arrays are relative to group g0)
+__global__ void k_pack_count(sphkv_store_t st, int T, int g0, const int8_t* __restrict__ z,
                              const int16_t* __restrict__ tier, int* counts, int* err) {
   __shared__ int c[SPHKV_MAX_TIERS];
   if (threadIdx.x < SPHKV_MAX_TIERS) c[threadIdx.x] = 0;
   __syncthreads();
-  const int64_t g = blockIdx.x;
+  const int64_t g = g0 + blockIdx.x;
   for (int i = threadIdx.x; i < T; i += blockDim.x) {
-    int64_t s = g * T + i;
+    int64_t s = (int64_t)blockIdx.x * T + i;
     if (z[s] == 1) {
       int ti = tier_idx(st, tier[s]);
       if (ti <= 0) { atomicExch(err, 1); continue; }  // retained state at drop tier
@@ -238,7 +239,7 @@ __global__ void k_pack_ptrlen(sphkv_store_t st, const int* __restrict__ page_bas
 
 // per group: rank of each retained token inside its (group, tier) in token
 // order -> page_items[page * P + slot] = state index
-__global__ void __launch_bounds__(1024) k_pack_rank(sphkv_store_t st, int T,
+__global__ void __launch_bounds__(1024) k_pack_rank(sphkv_store_t st, int T, int g0,
                                                     const int8_t* __restrict__ z,
                                                     const int16_t* __restrict__ tier,
                                                     const int* __restrict__ page_base,
@@ -246,14 +247,14 @@ __global__ void __launch_bounds__(1024) k_pack_rank(sphkv_store_t st, int T,
   __shared__ int wc[32][SPHKV_MAX_TIERS];
   __shared__ int running[SPHKV_MAX_TIERS];
   const int NT = st.n_tiers;
-  const int64_t g = blockIdx.x;
+  const int64_t gr = blockIdx.x, g = g0 + gr;  // relative / absolute group
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x < SPHKV_MAX_TIERS) running[threadIdx.x] = 0;
   __syncthreads();
   for (int base = 0; base < T; base += blockDim.x) {
     const int i = base + threadIdx.x;
     int ti = -1;
-    if (i < T && z[g * T + i] == 1) ti = tier_idx(st, tier[g * T + i]);
+    if (i < T && z[gr * T + i] == 1) ti = tier_idx(st, tier[gr * T + i]);
     int my_rank_in_warp = 0;
     for (int t = 1; t < NT; ++t) {
       unsigned m = __ballot_sync(0xffffffffu, ti == t);
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(1024) k_pack_rank(sphkv_store_t st, int T,
       int r = running[ti] + my_rank_in_warp;
       for (int w = 0; w < warp; ++w) r += wc[w][ti];
       int pid = page_base[g * NT + ti] + r / st.page_size;
-      page_items[(int64_t)(pid - first) * st.page_size + r % st.page_size] = (int)(g * T + i);
+      page_items[(int64_t)(pid - first) * st.page_size + r % st.page_size] = (int)(gr * T + i);
     }
     __syncthreads();
     if (threadIdx.x < NT && threadIdx.x > 0) {
@@ -706,9 +707,8 @@ __global__ void k_import(sphkv_store_t st, const int64_t* __restrict__ offsets,
 
 // dense baseline store: bf16 K and fp16 V pages, swizzled rows
 template <typename T>
-__global__ void k_dense_fill(sphkv_dense_store_t st, const T* __restrict__ keys,
-                             const uint16_t* __restrict__ values) {
-  const int64_t groups = (int64_t)st.batch * st.layers * st.heads;
+__global__ void k_dense_fill(sphkv_dense_store_t st, int64_t g0, int64_t groups,
+                             const T* __restrict__ keys, const uint16_t* __restrict__ values) {
   const int dp = (st.d + 15) / 16 * 16, dvp = (st.d_v + 15) / 16 * 16;
   const int64_t per_group = (int64_t)st.n_pages_per_group * st.page_size;
   const int64_t n = groups * per_group;
@@ -717,14 +717,15 @@ __global__ void k_dense_fill(sphkv_dense_store_t st, const T* __restrict__ keys,
     const int64_t g = it / per_group, pos = it % per_group;
     const int i = (int)(pos % st.page_size);
     const bool valid = pos < st.tokens;
-    const int64_t src = g * st.tokens + pos;
-    uint16_t* krow = st.keys + (it - i) * dp;
+    const int64_t src = g * st.tokens + pos;  // relative to group g0
+    const int64_t dst = it + g0 * per_group;
+    uint16_t* krow = st.keys + (dst - i) * dp;
     for (int e = 0; e < dp; ++e) {
       float v = (valid && e < st.d) ? (float)load_as_double(keys + src * st.d + e) : 0.f;
       __nv_bfloat16 h = __float2bfloat16_rn(v);
       krow[vswz(i, e, dp)] = *reinterpret_cast<uint16_t*>(&h);
     }
-    uint16_t* vrow = st.values + (it - i) * dvp;
+    uint16_t* vrow = st.values + (dst - i) * dvp;
     for (int e = 0; e < dvp; ++e)
       vrow[vswz(i, e, dvp)] = (valid && e < st.d_v) ? values[src * st.d_v + e] : (uint16_t)0;
   }
@@ -835,20 +836,26 @@ extern "C" int64_t sphkv_pack_workspace_bytes(int batch, int layers, int heads, 
   return 256 + e * 4 * 2 + e * 8 + 64 + (groups * tokens + groups * SPHKV_MAX_TIERS * 1024) * 4;
 }
 
-extern "C" int sphkv_pack_pages(const sphkv_store_t* st, const void* keys, int key_dtype,
-                                const double* angles, const double* radii, const uint16_t* values,
-                                const int8_t* z, const int16_t* tier, const uint8_t* protect,
-                                int tokens, void* workspace, int64_t workspace_bytes,
-                                cudaStream_t stream) {
+extern "C" int sphkv_pack_pages_groups(const sphkv_store_t* st, int group0, int n_groups,
+                                       const void* keys, int key_dtype, const double* angles,
+                                       const double* radii, const uint16_t* values,
+                                       const int8_t* z, const int16_t* tier,
+                                       const uint8_t* protect, int tokens, void* workspace,
+                                       int64_t workspace_bytes, cudaStream_t stream) {
   if (int e = validate_store(st)) return e;
   if (!radii || !values || !z || !tier || !protect || !workspace)
     return fail(SPHKV_E_VALUE, "null argument");
   if (!angles && (!keys || check_dtype(key_dtype))) return fail(SPHKV_E_VALUE, "need keys or angles");
   const int groups = st->batch * st->layers * st->heads;
+  if (group0 < 0 || n_groups < 0 || group0 + n_groups > groups)
+    return fail(SPHKV_E_KEY, "groups [%d, %d) outside the store's %d", group0, group0 + n_groups,
+                groups);
+  if (n_groups == 0) return SPHKV_OK;
   const int NT = st->n_tiers;
   const int P = st->page_size;
   if (groups * NT > 1023 * 64) return fail(SPHKV_E_UNSUPPORTED, "too many (group, tier) entries");
   int64_t need = sphkv_pack_workspace_bytes(st->batch, st->layers, st->heads, tokens);
+  need -= (int64_t)(groups - n_groups) * tokens * 4;  // page_items of the packed groups only
   if (workspace_bytes < need) return fail(SPHKV_E_VALUE, "pack workspace too small (%lld < %lld)",
                                           (long long)workspace_bytes, (long long)need);
   uint8_t* ws = (uint8_t*)workspace;
@@ -864,7 +871,7 @@ extern "C" int sphkv_pack_pages(const sphkv_store_t* st, const void* keys, int k
   // read the current page count (fresh stores: 0) for the page range we write
   uint64_t host_counters[2];
   SPHKV_CUDA_TRY(cudaMemcpyAsync(host_counters, st->counters, 16, cudaMemcpyDeviceToHost, stream));
-  k_pack_count<<<groups, 256, 0, stream>>>(*st, tokens, z, tier, counts, err);
+  k_pack_count<<<n_groups, 256, 0, stream>>>(*st, tokens, group0, z, tier, counts, err);
   SPHKV_LAUNCH_CHECK();
   k_pack_plan<<<1, 1023, 0, stream>>>(*st, counts, page_base, code_base, err);
   SPHKV_LAUNCH_CHECK();
@@ -883,7 +890,8 @@ extern "C" int sphkv_pack_pages(const sphkv_store_t* st, const void* keys, int k
   const int first = (int)host_counters[0];
   const int n_new = (int)(after[0] - host_counters[0]);
   if (n_new == 0) return SPHKV_OK;
-  k_pack_rank<<<groups, 1024, 0, stream>>>(*st, tokens, z, tier, page_base, first, page_items);
+  k_pack_rank<<<n_groups, 1024, 0, stream>>>(*st, tokens, group0, z, tier, page_base, first,
+                                             page_items);
   SPHKV_LAUNCH_CHECK();
   k_pack_scale<<<n_new, 128, 0, stream>>>(*st, first, n_new, page_items, radii);
   SPHKV_LAUNCH_CHECK();
@@ -902,6 +910,17 @@ extern "C" int sphkv_pack_pages(const sphkv_store_t* st, const void* keys, int k
   }
   SPHKV_LAUNCH_CHECK();
   return SPHKV_OK;
+}
+
+extern "C" int sphkv_pack_pages(const sphkv_store_t* st, const void* keys, int key_dtype,
+                                const double* angles, const double* radii, const uint16_t* values,
+                                const int8_t* z, const int16_t* tier, const uint8_t* protect,
+                                int tokens, void* workspace, int64_t workspace_bytes,
+                                cudaStream_t stream) {
+  if (!st) return fail(SPHKV_E_VALUE, "null argument");
+  return sphkv_pack_pages_groups(st, 0, st->batch * st->layers * st->heads, keys, key_dtype,
+                                 angles, radii, values, z, tier, protect, tokens, workspace,
+                                 workspace_bytes, stream);
 }
 
 extern "C" int64_t sphkv_append_workspace_bytes(int groups) {
@@ -983,18 +1002,32 @@ extern "C" int sphkv_import_streams(const sphkv_store_t* st, int n_pages, const 
   return SPHKV_OK;
 }
 
-extern "C" int sphkv_dense_fill(const sphkv_dense_store_t* st, const void* keys, int key_dtype,
-                                const uint16_t* values, cudaStream_t stream) {
+extern "C" int sphkv_dense_fill_groups(const sphkv_dense_store_t* st, int group0, int n_groups,
+                                       const void* keys, int key_dtype, const uint16_t* values,
+                                       cudaStream_t stream) {
   if (!st || !keys || !values) return fail(SPHKV_E_VALUE, "null argument");
   if (check_dtype(key_dtype)) return SPHKV_E_VALUE;
+  const int groups = st->batch * st->layers * st->heads;
+  if (group0 < 0 || n_groups < 0 || group0 + n_groups > groups)
+    return fail(SPHKV_E_KEY, "groups [%d, %d) outside the store's %d", group0, group0 + n_groups,
+                groups);
+  if (n_groups == 0) return SPHKV_OK;
+  const int64_t g0 = group0, ng = n_groups;
   switch (key_dtype) {
-    case SPHKV_F32: k_dense_fill<float><<<4 * SM_COUNT, 256, 0, stream>>>(*st, (const float*)keys, values); break;
-    case SPHKV_F64: k_dense_fill<double><<<4 * SM_COUNT, 256, 0, stream>>>(*st, (const double*)keys, values); break;
-    case SPHKV_BF16: k_dense_fill<__nv_bfloat16><<<4 * SM_COUNT, 256, 0, stream>>>(*st, (const __nv_bfloat16*)keys, values); break;
-    default: k_dense_fill<__half><<<4 * SM_COUNT, 256, 0, stream>>>(*st, (const __half*)keys, values); break;
+    case SPHKV_F32: k_dense_fill<float><<<4 * SM_COUNT, 256, 0, stream>>>(*st, g0, ng, (const float*)keys, values); break;
+    case SPHKV_F64: k_dense_fill<double><<<4 * SM_COUNT, 256, 0, stream>>>(*st, g0, ng, (const double*)keys, values); break;
+    case SPHKV_BF16: k_dense_fill<__nv_bfloat16><<<4 * SM_COUNT, 256, 0, stream>>>(*st, g0, ng, (const __nv_bfloat16*)keys, values); break;
+    default: k_dense_fill<__half><<<4 * SM_COUNT, 256, 0, stream>>>(*st, g0, ng, (const __half*)keys, values); break;
   }
   SPHKV_LAUNCH_CHECK();
   return SPHKV_OK;
+}
+
+extern "C" int sphkv_dense_fill(const sphkv_dense_store_t* st, const void* keys, int key_dtype,
+                                const uint16_t* values, cudaStream_t stream) {
+  if (!st) return fail(SPHKV_E_VALUE, "null argument");
+  return sphkv_dense_fill_groups(st, 0, st->batch * st->layers * st->heads, keys, key_dtype,
+                                 values, stream);
 }
 
 namespace sphkv {

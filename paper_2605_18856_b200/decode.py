@@ -87,7 +87,9 @@ def ada_decode(store, q, plan: DecodePlan | None = None, *, out=None, partials=N
 
 
 def dense_decode(dstore, q, plan: DecodePlan | None = None, *, out=None, partials=None,
-                 stream=None):
+                 stream=None, token_begin=0):
+    """Dense bf16 paged decode (decode.py:63-69, 302-307); `token_begin` > 0
+    attends only tokens >= token_begin (a sliding-window layer)."""
     import torch
 
     l = _lib.require_gpu()
@@ -100,10 +102,10 @@ def dense_decode(dstore, q, plan: DecodePlan | None = None, *, out=None, partial
     if out is None:
         out = torch.empty((ng * G, dstore.d_v), dtype=torch.float32, device="cuda")
     sp = _lib.stream_ptr(stream)
-    _lib.check(l.sphkv_dense_decode_fused(
+    _lib.check(l.sphkv_dense_decode_window(
         dstore.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units, partials.data_ptr(),
         plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng, plan.ctl.data_ptr(),
-        out.data_ptr(), int(plan.dynamic), plan.grid, sp))
+        out.data_ptr(), int(plan.dynamic), int(token_begin), plan.grid, sp))
     return out
 
 

@@ -226,7 +226,8 @@ class PagedStore:
 
     def __init__(self, tiers: TierTable, layers: int, heads: int, d: int, d_v: int,
                  page_size: int, meter: TrafficMeter | None = None, *, batch: int = 1,
-                 capacity_tokens: int = 1024, append_tokens: int = 256):
+                 capacity_tokens: int = 1024, append_tokens: int = 256,
+                 max_pages: int | None = None, code_bytes: int | None = None):
         import torch
 
         if page_size < 1:
@@ -252,6 +253,13 @@ class PagedStore:
         max_block = max(code_block_bytes(d, page_size, t.angle_bits, t.radius_bits)
                         for t in tiers.non_drop)
         self.code_cap = self.max_pages * max_block + 256
+        # explicit pool sizes (a caller that knows the allocation, e.g. the
+        # benchmark: the worst case -- every item at the widest tier -- does
+        # not fit a 128K-token batch in HBM)
+        if max_pages is not None:
+            self.max_pages = max(int(max_pages), 1)
+        if code_bytes is not None:
+            self.code_cap = int(code_bytes) + 256
         dev = "cuda"
         self.t_pages = torch.zeros(self.max_pages * 32, dtype=torch.uint8, device=dev)
         self.t_ptr = torch.zeros(self.groups * self.ptr_cap, dtype=torch.int32, device=dev)
@@ -598,14 +606,13 @@ class PagedStore:
         return total
 
     def stream_bytes_total(self):
-        """Algorithmic decode bytes of one full pass over every group (8(d))."""
+        """Algorithmic decode bytes of one full pass over every group (8(d)):
+        per page header + packed code streams + fp16 values (store.py:315-322)."""
         n, rows, _, _ = self._host()
-        total = PAGE_HEADER_BYTES * n
-        for r in rows:
-            t = self.tiers.spec_for(int(r["tier"]))
-            a, b, v, *_ = _page_formulas(int(r["count"]), self.page_size, t, self.d, self.d_v)
-            total += a + b + v
-        return total
+        c = rows["count"].astype(np.int64)
+        a = (c * (self.d - 1) * rows["abits"].astype(np.int64) + 7) // 8
+        b = (c * rows["rbits"].astype(np.int64) + 7) // 8
+        return int(PAGE_HEADER_BYTES * n + a.sum() + b.sum() + (c * self.d_v * 2).sum())
 
     def resident_breakdown(self) -> ResidentBreakdown:
         n, rows, _, _ = self._host()
@@ -805,8 +812,11 @@ def pack_pages_arrays(assignment, radii, angles, values, tiers: TierTable, page_
 
 
 def pack_device(store: PagedStore, *, radii, values, z, tier, protect, tokens, angles=None,
-                keys=None):
-    """Device packer entry (tensors or arrays): encode + quantize + page layout."""
+                keys=None, groups=None):
+    """Device packer entry (tensors or arrays): encode + quantize + page layout.
+
+    `groups` = (first, count) packs only that contiguous group range (arrays
+    relative to it, e.g. one sequence of a batched store); default: all."""
     import torch
 
     l = _lib.require_gpu()
@@ -831,11 +841,14 @@ def pack_device(store: PagedStore, *, radii, values, z, tier, protect, tokens, a
     zz = dev(z, torch.int8)
     tt = dev(tier, torch.int16)
     pp = dev(protect, torch.uint8)
-    nbytes = l.sphkv_pack_workspace_bytes(store.batch, store.layers, store.heads, tokens)
+    g0, ng = (0, store.groups) if groups is None else (int(groups[0]), int(groups[1]))
+    nbytes = (l.sphkv_pack_workspace_bytes(store.batch, store.layers, store.heads, tokens)
+              - (store.groups - ng) * tokens * 4)
     ws = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-    _lib.check(l.sphkv_pack_pages(store.cptr, _lib.ptr(k), kd, _lib.ptr(a), r.data_ptr(),
-                                  v.data_ptr(), zz.data_ptr(), tt.data_ptr(), pp.data_ptr(),
-                                  tokens, ws.data_ptr(), nbytes, _lib.stream_ptr()))
+    _lib.check(l.sphkv_pack_pages_groups(store.cptr, g0, ng, _lib.ptr(k), kd, _lib.ptr(a),
+                                         r.data_ptr(), v.data_ptr(), zz.data_ptr(),
+                                         tt.data_ptr(), pp.data_ptr(), tokens, ws.data_ptr(),
+                                         nbytes, _lib.stream_ptr()))
     store._invalidate()
     store._refresh_lut()
     return store
@@ -854,8 +867,10 @@ class DenseStore:
         self.t_values = None
         self.cstruct = None
 
-    def bulk_load(self, keys, values, metered=False):
-        """keys (B*L*H, T, d) / (L, H, T, d); values likewise with d_v."""
+    def bulk_load(self, keys, values, metered=False, groups=None):
+        """keys (B*L*H, T, d) / (L, H, T, d); values likewise with d_v.
+        `groups` = (first, count): load only that contiguous group range (the
+        arrays then hold those groups only); the pools are sized on first use."""
         import torch
 
         l = _lib.require_gpu()
@@ -863,25 +878,32 @@ class DenseStore:
         v = values if isinstance(values, torch.Tensor) else torch.as_tensor(np.asarray(values), device="cuda")
         k = k.to("cuda").contiguous()
         v = _lib.to_f16(v)
-        groups = self.batch * self.layers * self.heads
-        T = k.numel() // (groups * self.d)
-        self.tokens = T
+        all_groups = self.batch * self.layers * self.heads
+        g0, ng = (0, all_groups) if groups is None else (int(groups[0]), int(groups[1]))
+        T = k.numel() // (ng * self.d)
         P = self.page_size
         npg = -(-T // P)
-        dp = (self.d + 15) // 16 * 16
-        dvp = (self.d_v + 15) // 16 * 16
-        self.t_keys = torch.zeros(groups * npg * P * dp, dtype=torch.bfloat16, device="cuda")
-        self.t_values = torch.zeros(groups * npg * P * dvp, dtype=torch.float16, device="cuda")
-        c = _lib.CDenseStore()
-        c.batch, c.layers, c.heads = self.batch, self.layers, self.heads
-        c.d, c.d_v, c.page_size = self.d, self.d_v, P
-        c.n_pages_per_group, c.tokens = npg, T
-        c.keys, c.values = self.t_keys.data_ptr(), self.t_values.data_ptr()
-        self.cstruct = c
+        if self.cstruct is None:
+            self.tokens = T
+            dp = (self.d + 15) // 16 * 16
+            dvp = (self.d_v + 15) // 16 * 16
+            self.t_keys = torch.zeros(all_groups * npg * P * dp, dtype=torch.bfloat16, device="cuda")
+            self.t_values = torch.zeros(all_groups * npg * P * dvp, dtype=torch.float16,
+                                        device="cuda")
+            c = _lib.CDenseStore()
+            c.batch, c.layers, c.heads = self.batch, self.layers, self.heads
+            c.d, c.d_v, c.page_size = self.d, self.d_v, P
+            c.n_pages_per_group, c.tokens = npg, T
+            c.keys, c.values = self.t_keys.data_ptr(), self.t_values.data_ptr()
+            self.cstruct = c
+        elif T != self.tokens:
+            raise ValueError(f"dense store holds {self.tokens} tokens per group, got {T}")
+        c = self.cstruct
+        groups = ng
         kd = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16,
               torch.float16: _lib.F16}[k.dtype]
-        _lib.check(l.sphkv_dense_fill(ctypes.byref(c), k.data_ptr(), kd, v.data_ptr(),
-                                      _lib.stream_ptr()))
+        _lib.check(l.sphkv_dense_fill_groups(ctypes.byref(c), g0, ng, k.data_ptr(), kd,
+                                             v.data_ptr(), _lib.stream_ptr()))
         if metered:
             for _ in range(groups):
                 pages = npg
