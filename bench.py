@@ -433,6 +433,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no graphs (for ncu)")
+    ap.add_argument("--hbyte", action="store_true",
+                    help="2-bit tier through the per-query h-byte tables (csrc/hb_tile.cuh)")
     ap.add_argument("--units-per-cta", type=int, default=1)
     ap.add_argument("--tail", type=float, default=0.0,
                     help="fraction of each CTA's share cut into small dynamically claimed units")
@@ -486,6 +488,7 @@ def main():
                        dense=not args.no_dense, reduction=args.reduction,
                        parity=not args.no_parity and rank == 0)
     st, ds, q = W["st"], W["ds"], W["q"]
+    st.hbyte_tables = args.hbyte
     pairs = set(W["pairs"])
     log("setup", json.dumps(W["timings"]), json.dumps(W["info"]))
 
@@ -520,11 +523,11 @@ def main():
         for l, p in enumerate(plans):
             if fused:
                 _lib.check(lib.sphkv_ada_decode_fused(
-                    st.cptr, q.data_ptr(), G, p.units.data_ptr(), p.n_units, parts[l].data_ptr(),
+                    st.cptr_for(G), q.data_ptr(), G, p.units.data_ptr(), p.n_units, parts[l].data_ptr(),
                     p.slot_group.data_ptr(), p.slot_begin.data_ptr(), len(p.group_ids),
                     p.ctl.data_ptr(), outs[l].data_ptr(), int(p.dynamic), p.grid, sp))
                 continue
-            _lib.check(lib.sphkv_ada_decode(st.cptr, q.data_ptr(), G, p.units.data_ptr(),
+            _lib.check(lib.sphkv_ada_decode(st.cptr_for(G), q.data_ptr(), G, p.units.data_ptr(),
                                             p.n_units, parts[l].data_ptr(), None, None, p.grid, sp))
             if with_merge and mode != "split":
                 _lib.check(lib.sphkv_lse_merge(parts[l].data_ptr(), p.slot_begin.data_ptr(),

@@ -85,7 +85,9 @@ typedef struct {
   int32_t n_tiers;            /* entries in `tiers`, drop tier first          */
   int32_t max_pages;          /* capacity of the page-indexed pools          */
   int32_t ptr_cap;            /* pointer-list capacity per group             */
-  int32_t _pad;
+  int32_t lut_flags;          /* bit 0: the prebuilt LUT omits the 2-bit tier,
+                                 which decodes from per-query h-byte tables
+                                 (launches with G <= 4 query heads, d = 64/128) */
   uint64_t code_cap;          /* bytes in `codes`                             */
   sphkv_tier_t tiers[SPHKV_MAX_TIERS];
   sphkv_page_t* pages;        /* [max_pages]                                  */

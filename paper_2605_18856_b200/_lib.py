@@ -40,7 +40,7 @@ class CTier(ctypes.Structure):
 class CStore(ctypes.Structure):
     _fields_ = [("batch", c_int32), ("layers", c_int32), ("heads", c_int32), ("d", c_int32),
                 ("d_v", c_int32), ("page_size", c_int32), ("n_tiers", c_int32),
-                ("max_pages", c_int32), ("ptr_cap", c_int32), ("_pad", c_int32),
+                ("max_pages", c_int32), ("ptr_cap", c_int32), ("lut_flags", c_int32),
                 ("code_cap", c_uint64), ("tiers", CTier * MAX_TIERS),
                 ("pages", c_void_p), ("ptr", c_void_p), ("ptr_len", c_void_p),
                 ("group_last", c_void_p), ("codes", c_void_p), ("values", c_void_p),
@@ -116,6 +116,8 @@ def _declare(lib):
         "sphkv_dense_store_logits": (c_int, [vp, vp, i, i, vp, vp]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("SPHKV_LIB") and not hasattr(lib, name):
+            continue  # experiment builds (SPHKV_LIB) may predate newer entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -61,9 +61,13 @@ __host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c
 // first; without them the fixed priority below applies.  Quad tables are
 // always replicated; single-code tiers of 8..12 bits fall back to two copies
 // when full replication (16 copies) does not fit.
+// hb != 0: the 2-bit tier decodes from per-query h-byte tables (hb_tile.cuh)
+// and gets no shared-memory table here.  budget: LUT bytes (0 = default).
 __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n_tiers,
                                                 int off[SPHKV_MAX_TIERS],
-                                                const int64_t* items = nullptr) {
+                                                const int64_t* items = nullptr, int hb = 0,
+                                                int budget = 0) {
+  const int LUT_BUDGET = budget > 0 ? budget : LUT_BUDGET_BYTES;
   int mode[SPHKV_MAX_TIERS];
   bool known = false;
   if (items != nullptr)
@@ -77,7 +81,8 @@ __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n
     const int b = tiers[t].angle_bits;
     const bool quad = lut_group(b) == 4;
     if (known && items[t] == 0) continue;
-    if (b <= LUT_MAX_BITS && total + lut_bytes(b, quad ? 8 : 1) <= LUT_BUDGET_BYTES) {
+    if (hb && b == 2) continue;
+    if (b <= LUT_MAX_BITS && total + lut_bytes(b, quad ? 8 : 1) <= LUT_BUDGET) {
       total += lut_bytes(b, quad ? 8 : 1);
       off[t] = 0;  // has a table; placed below
       mode[t] = quad ? 1 : 0;
@@ -87,12 +92,12 @@ __host__ __device__ inline int lut_layout_tiers(const sphkv_tier_t* tiers, int n
     const int b = tiers[t].angle_bits;
     if (off[t] != 0 || mode[t] != 0) return;
     const int extra = lut_bytes(b, lut_copies(b, 1)) - lut_bytes(b, 1);
-    if (total + extra <= LUT_BUDGET_BYTES) {
+    if (total + extra <= LUT_BUDGET) {
       mode[t] = 1;
       total += extra;
     } else if (b >= 8) {
       const int extra2 = lut_bytes(b, 2) - lut_bytes(b, 1);
-      if (total + extra2 <= LUT_BUDGET_BYTES) {
+      if (total + extra2 <= LUT_BUDGET) {
         mode[t] = 2;
         total += extra2;
       }
@@ -554,11 +559,17 @@ __device__ __noinline__ void ada_tile_generic(const uint8_t* __restrict__ blk, i
 
 // Logits (base 2) of the tile's items sub*128 + 32 k + lane, k < 4, G heads.
 // lut_enc: (table byte offset << 2) | mode, or -1 (no table).
+template <int D, int GP>
+__device__ __noinline__ void ada_tile_hb(const uint8_t* __restrict__ blkb, int sub, int lane,
+                                         uint32_t hb, uint32_t rbit0, int rb, float rscale,
+                                         float lg[TK][2 * GP]);
+
+// hb_off: byte offset of the per-query 2-bit h-byte tables in `sm` (0: none)
 template <int GP>
 __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, int d, int P,
                                                    const sphkv_page_t& pg, int sub, int lane,
                                                    const uint8_t* sm, uint32_t qs, int lut_enc,
-                                                   float lg[TK][2 * GP]) {
+                                                   float lg[TK][2 * GP], uint32_t hb_off = 0) {
   const uint8_t* blk = codes + pg.code_off;
   const uint32_t rbit0 = (uint32_t)(angle_part_bytes(d, P, B) * 8);
   const int rb = pg.rbits;
@@ -568,6 +579,16 @@ __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, 
   const uint32_t tb = has ? (uint32_t)(lut_enc >> 2) : 0u;
 #define SPHKV_WI(b, dd, mode, rp) \
   ada_tile_wi<b, dd, GP, mode, rp>(blk, sub, lane, sm, qs, tb, rbit0, rb, rs, lg)
+#ifndef SPHKV_NO_HB
+  if constexpr (GP <= 2) {
+    if (B == 2 && hb_off != 0 && P % TTI == 0) {
+      const uint32_t hb = ptx::smem_u32(sm) + hb_off;
+      if (d == 128) ada_tile_hb<128, GP>(blk, sub, lane, hb, rbit0, rb, rs, lg);
+      else ada_tile_hb<64, GP>(blk, sub, lane, hb, rbit0, rb, rs, lg);
+      return;
+    }
+  }
+#endif
   if (P % TTI != 0) {
     // pages narrower than a tile: generic path (guards items >= P)
   } else if (d == 128) {

@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "ptx.cuh"
 #include "ada_tile.cuh"
+#include "hb_tile.cuh"
 
 namespace sphkv {
 
@@ -81,6 +82,8 @@ struct AdaParams {
   int TI;                   // tile items (min(P, 128))
   int dvp;                  // d_v padded to 16
   uint32_t smem_q, smem_tiles, smem_p, smem_v, smem_bar;  // byte offsets
+  uint32_t smem_hb;         // per-query 2-bit h-byte tables (hb_tile.cuh), if hb
+  int hb;                   // 2-bit tier decodes through the h-byte tables
   int pslot_bytes, prow_bytes, prows;  // P slot: prows rows of TI fp16 weights + header
   FusedCtl fz;
 };
@@ -497,7 +500,6 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   extern __shared__ __align__(128) uint8_t smem[];
   const sphkv_store_t& st = p.st;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float2* lut = reinterpret_cast<float2*>(smem);
   float2* qs = reinterpret_cast<float2*>(smem + p.smem_q);
   TileEntry* tiles = reinterpret_cast<TileEntry*>(smem + p.smem_tiles);
   // seg[0] = tiles of the current segment, seg[1] = its end pointer position,
@@ -561,6 +563,23 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 #endif
     }
   };
+#ifndef SPHKV_PF_L1
+#define SPHKV_PF_L1 6
+#endif
+  // h-byte tiles load their whole 4 KB code block up front: pull tile t's
+  // block into this SM's L1 (one 128-byte line per lane) about one tile-time
+  // ahead, so whichever warp claims it finds it there.
+  auto prefetch_tile_l1 = [&](int t, int nt) {
+    if (SPHKV_PF_L1 > 0 && p.hb && t < nt) {
+      const TileEntry tn = tiles[t];
+      const sphkv_page_t pn = st.pages[tn.page];
+      if (pn.abits == 2) {
+        const uint64_t W4 = (uint64_t)item_words(d, 2) * 128;
+        const uint8_t* b = st.codes + pn.code_off + (uint64_t)((tn.sub_off >> 24) * TI / 32) * W4;
+        if ((uint32_t)lane * 128u < (uint32_t)(TI / 32) * (uint32_t)W4) ptx::prefetch_l1_line(b + lane * 128);
+      }
+    }
+  };
   // Also independent of the previous grid (it only reads q and writes
   // outputs): the first unit's tile list and its first L2 prefetches.
   // scalars of the fused merge / unit queue live after the barriers (no static
@@ -617,23 +636,35 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       float b = (2 * g2 + 1 < p.G) ? qg[(size_t)(2 * g2 + 1) * d + j] * qscale : 0.f;
       qs[j * (q_row_bytes(GP) / 8) + g2] = make_float2(a, b);
     }
-    PVState<ADA_MTW> s;
-    if (warp >= ADA_NL) pv_init(s);
-    // a unit runs as one or more segments of <= MAX_UNIT_TILES tiles; the
-    // online-softmax state of the PV warps carries across segments
-    for (bool seg_first = true;; seg_first = false) {
-      if (!(first && seg_first) && warp == 0) {
-        const int pb = seg_first ? unit.ptr_begin : seg[1];
-        const int ib = seg_first ? 0 : seg[2];
-        __syncwarp();  // every lane has read seg[] before lane 0 rewrites it
-        build_tiles(st, unit.group, pb, unit.ptr_end, ib, TI, tiles, seg, lane);
-        if (lane == 0) *tile_ctr = 0;
+#ifndef SPHKV_NO_HB
+    if constexpr (GP <= 2) {
+      if (p.hb) {  // per-query tables of the 2-bit tier; scratch = the idle P slots
+        __syncthreads();  // the previous unit's last P-slot reads are done
+        double* scratch = reinterpret_cast<double*>(pslots);
+        const double qs_d = 1.4426950408889634 / sqrt((double)d);
+        if (d == 128)
+          hb_build<128>(smem + p.smem_hb, scratch, qg, p.G, qs_d);
+        else
+          hb_build<64>(smem + p.smem_hb, scratch, qg, p.G, qs_d);
       }
-      __syncthreads();
-      const int nt = seg[0], seg_end = seg[1];  // read before warp 0 may rebuild
-
-      if (warp < ADA_NL) {
-        // ---------------- logit warps ----------------
+    }
+#endif
+    // A unit runs as one or more segments of <= MAX_UNIT_TILES tiles.  The
+    // logit and PV warps run their own segment loops (separate register
+    // sets: the PV warps' online-softmax state lives only in theirs) that meet
+    // at the same two block barriers per segment.
+    if (warp < ADA_NL) {
+      // ---------------- logit warps ----------------
+      for (bool seg_first = true;; seg_first = false) {
+        if (!(first && seg_first) && warp == 0) {
+          const int pb = seg_first ? unit.ptr_begin : seg[1];
+          const int ib = seg_first ? 0 : seg[2];
+          __syncwarp();  // every lane has read seg[] before lane 0 rewrites it
+          build_tiles(st, unit.group, pb, unit.ptr_end, ib, TI, tiles, seg, lane);
+          if (lane == 0) *tile_ctr = 0;
+        }
+        __syncthreads();
+        const int nt = seg[0], seg_end = seg[1];  // read before warp 0 may rebuild
         if (!lut_ready) {
           ptx::mbar_wait(lut_bar, 0);
           lut_ready = true;
@@ -649,6 +680,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
           k = __shfl_sync(0xffffffffu, k, 0);
           if (k >= nt) break;
           prefetch_tile(k + SPHKV_PF_DIST, nt);
+          prefetch_tile_l1(k + SPHKV_PF_L1, nt);
           const uint32_t gk = gbase + k;
           const TileEntry te = tiles[k];
           const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
@@ -660,7 +692,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
             for (int b_ = 0; b_ < 2 * GP; ++b_) lg[a_][b_] = (float)(a_ + b_) * 0.01f + (float)ti;
 #else
           ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
-                                 p.lut_off[ti], lg);
+                                 p.lut_off[ti], lg, p.hb ? p.smem_hb : 0u);
 #endif
           uint32_t valid = 0;
 #pragma unroll
@@ -684,14 +716,23 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
         }
-      } else {
-        // ---------------- PV warps ----------------
-        // NPV warps split the d_v m-tiles; all consume every tile in order.
-        // Lane 0 of PV warp 0 is also the V producer: it refills slot vs once
-        // every PV warp has released it (v_empty counts NPV arrivals).
+        gbase += nt;
+        __syncthreads();  // the tile list and seg[] may be rebuilt now
+        if (seg_end >= unit.ptr_end) break;
+      }
+    } else {
+      // ---------------- PV warps ----------------
+      // NPV warps split the d_v m-tiles; all consume every tile in order.
+      // Lane 0 of PV warp 0 is also the V producer: it refills slot vs once
+      // every PV warp has released it (v_empty counts NPV arrivals).
+      PVState<ADA_MTW> s;
+      pv_init(s);
+      const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
+      for (bool seg_first = true;; seg_first = false) {
+        __syncthreads();
+        const int nt = seg[0], seg_end = seg[1];
         if (!(first && seg_first) && pw == 0 && lane == 0)
           for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k, gbase);
-        const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
         for (int k = 0; k < nt; ++k) {
           const uint32_t gk = gbase + k;
           const int vs = gk % ADA_NV, ps = gk % ADA_NS;
@@ -713,12 +754,10 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
             if (pw == 0 && k + ADA_NV < nt) issue_v(k + ADA_NV, gbase);
           }
         }
+        gbase += nt;
+        __syncthreads();
+        if (seg_end >= unit.ptr_end) break;
       }
-      gbase += nt;
-      __syncthreads();  // the tile list and seg[] may be rebuilt now
-      if (seg_end >= unit.ptr_end) break;
-    }
-    if (warp >= ADA_NL) {
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
       pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane,
                         p.fz.top2 != nullptr ? p.fz.top2 + (size_t)unit.out_slot * p.G : nullptr);
@@ -988,8 +1027,42 @@ static size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 extern "C" int64_t sphkv_partial_floats(int G, int d_v) { return (int64_t)G * (d_v + 2); }
 
-static int lut_layout(const sphkv_store_t* st, int off[SPHKV_MAX_TIERS]) {
-  return lut_layout_tiers(st->tiers, st->n_tiers, off, st->lut_items);
+// Shared memory of a GP <= 2 launch besides the LUT and the h-byte tables
+// (q rows, tile list, P slots, V ring, barriers), rounded up.
+static size_t ada_other_smem(int d, int d_v, int P) {
+  const int TI = P < ADA_TI ? P : ADA_TI;
+  const size_t dvp = (size_t)(d_v + 15) / 16 * 16;
+  const size_t prow = (size_t)TI * 2 + PROW_PAD;
+  return (size_t)d * q_row_bytes(2) + MAX_UNIT_TILES * sizeof(TileEntry) + 16 +
+         ADA_NS * ((4 * prow + 96 + 15) / 16 * 16) + ADA_NV * TI * dvp * 2 + 1024 + 4 * 128;
+}
+
+// Does this launch decode the 2-bit tier through the h-byte tables?  The
+// caller opts in per store (lut_flags bit 0, with the matching prebuilt LUT);
+// launches outside the mode's limits (G > 4, other d, narrow pages) use the
+// quad-row table (in-kernel LUT fill if the prebuilt one is the h-byte layout).
+static bool ada_use_hb(const sphkv_store_t* st, int GP) {
+#ifdef SPHKV_NO_HB  // experiment builds: the 2-bit tier through the quad-row table
+  return false;
+#endif
+  if (!(st->lut_flags & 1)) return false;
+  if (GP > 2 || !hb_supported(st->d) || st->page_size % ADA_TI != 0) return false;
+  for (int t = 1; t < st->n_tiers; ++t)
+    if (st->tiers[t].angle_bits == 2) return true;
+  return false;
+}
+
+// LUT placement for a launch mode: the h-byte mode drops the 2-bit table and
+// gives the LUT what the h-byte tables leave of the opt-in shared memory.
+static int lut_layout(const sphkv_store_t* st, int off[SPHKV_MAX_TIERS], int hb) {
+  int budget = 0;
+  if (hb) {
+    const long left = 232448L - (long)hb_bytes(st->d) - (long)ada_other_smem(st->d, st->d_v,
+                                                                             st->page_size);
+    budget = (int)(left < LUT_BUDGET_BYTES ? (left / 16) * 16 : LUT_BUDGET_BYTES);
+    if (budget < 16) budget = 16;
+  }
+  return lut_layout_tiers(st->tiers, st->n_tiers, off, st->lut_items, hb, budget);
 }
 
 namespace sphkv {
@@ -1004,12 +1077,12 @@ extern "C" int sphkv_unit_tile_cap(void) { return MAX_UNIT_TILES; }
 
 extern "C" int64_t sphkv_lut_floats(const sphkv_store_t* st) {
   int off[SPHKV_MAX_TIERS];
-  return lut_layout(st, off) / 4 + 4;
+  return lut_layout(st, off, st->lut_flags & 1) / 4 + 4;
 }
 
 extern "C" int sphkv_store_build_lut(sphkv_store_t* st, cudaStream_t stream) {
   if (!st || !st->lut) return fail(SPHKV_E_VALUE, "store lut buffer missing");
-  int used = lut_layout(st, st->lut_off);
+  int used = lut_layout(st, st->lut_off, st->lut_flags & 1);
   if (used == 0) return SPHKV_OK;
   k_build_lut<<<64, 256, 0, stream>>>(*st);
   SPHKV_LAUNCH_CHECK();
@@ -1083,16 +1156,22 @@ static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
   p.fz = fz;
   p.TI = st->page_size < ADA_TI ? st->page_size : ADA_TI;
   p.dvp = (st->d_v + 15) / 16 * 16;
-  int used = lut_layout(st, p.lut_off);
+  const int GP = (G + 1) / 2;
+  p.hb = ada_use_hb(st, GP) ? 1 : 0;
+  int used = lut_layout(st, p.lut_off, p.hb);
   p.lut_bytes = used;
   p.lut_global = nullptr;
-  if (st->lut != nullptr) {
+  if (st->lut != nullptr && (st->lut_flags & 1) == p.hb) {
     bool same = true;
     for (int t = 0; t < SPHKV_MAX_TIERS; ++t) same = same && (st->lut_off[t] == p.lut_off[t]);
     if (same) p.lut_global = reinterpret_cast<const uint8_t*>(st->lut);
   }
-  const int GP = (G + 1) / 2;
   size_t off = align_up((size_t)used, 128);
+  if (p.hb) {
+    if (off == 0) off = 128;  // smem_hb == 0 means "no tables" to the tile dispatch
+    p.smem_hb = (uint32_t)off;
+    off = align_up(off + hb_bytes(st->d), 128);
+  }
   p.smem_q = (uint32_t)off;
   off = align_up(off + (size_t)st->d * q_row_bytes(GP), 128);
   p.smem_tiles = (uint32_t)off;
@@ -1108,7 +1187,7 @@ static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
   p.smem_bar = (uint32_t)off;
   off += (2 * ADA_NS + 2 * ADA_NV + 1) * 8 + 8 + 64;  // barriers, s_flag/s_next, s_ml[16]
   size_t smem = off;
-  if (smem > 227 * 1024) return fail(SPHKV_E_UNSUPPORTED, "ADA smem %zu exceeds 227 KB", smem);
+  if (smem > 232448) return fail(SPHKV_E_UNSUPPORTED, "ADA smem %zu exceeds 227 KB", smem);
   if (grid <= 0) grid = SM_COUNT;
   if (grid > n_units) grid = n_units;
 #ifdef SPHKV_ONLY_GP  // fast experimental builds: one GQA width only

@@ -67,18 +67,18 @@ def ada_decode(store, q, plan: DecodePlan | None = None, *, out=None, partials=N
         assert margins.dtype == torch.float32 and margins.numel() == ng * G
         top2 = torch.empty((plan.n_slots + 1) * G, dtype=torch.float32, device="cuda")
         _lib.check(l.sphkv_ada_decode_margins(
-            store.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
+            store.cptr_for(G), q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
             partials.data_ptr(), plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng,
             plan.ctl.data_ptr(), out.data_ptr(), int(plan.dynamic), top2.data_ptr(),
             margins.data_ptr(), plan.grid, sp))
         return out
     if logits is None:  # one launch: the last split of each group merges it in-kernel
         _lib.check(l.sphkv_ada_decode_fused(
-            store.cptr, q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
+            store.cptr_for(G), q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
             partials.data_ptr(), plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng,
             plan.ctl.data_ptr(), out.data_ptr(), int(plan.dynamic), plan.grid, sp))
         return out
-    _lib.check(l.sphkv_ada_decode(store.cptr, q.data_ptr(), G, plan.units.data_ptr(),
+    _lib.check(l.sphkv_ada_decode(store.cptr_for(G), q.data_ptr(), G, plan.units.data_ptr(),
                                   plan.n_units, partials.data_ptr(), _lib.ptr(logits),
                                   plan.dbg_offsets.data_ptr(), plan.grid, sp))
     _lib.check(l.sphkv_lse_merge(partials.data_ptr(), plan.slot_begin.data_ptr(), ng, G,

@@ -285,6 +285,7 @@ class PagedStore:
         if old is not None:  # keep the table placement hint across pool growth
             for k in range(_lib.MAX_TIERS):
                 c.lut_items[k] = old.lut_items[k]
+            c.lut_flags = old.lut_flags
         c.batch, c.layers, c.heads = self.batch, self.layers, self.heads
         c.d, c.d_v, c.page_size = self.d, self.d_v, self.page_size
         c.n_tiers = len(self.tiers.tiers)
@@ -318,16 +319,55 @@ class PagedStore:
             self._build_lut()
 
     def _build_lut(self):
+        """(Re)build the prebuilt shared-memory tables for the current layout
+        hint and lut_flags; both variants (with / without the 2-bit table)
+        are cached so launches with different GQA widths do not rebuild."""
         import torch
 
         l = _lib.require_gpu()
         c = self.cstruct
         c.tiers = _lib.tiers_to_c(self.tiers)
+        key = (int(c.lut_flags), tuple(c.lut_items))
+        cache = self.__dict__.setdefault("_lut_cache", {})
+        if key in cache and cache[key][2] == self._lut_gen():
+            t, off, _ = cache[key]
+            c.lut = t.data_ptr()
+            for k in range(_lib.MAX_TIERS):
+                c.lut_off[k] = off[k]
+            return
         n = l.sphkv_lut_floats(ctypes.byref(c))
-        if self.t_lut is None or self.t_lut.numel() < n:
-            self.t_lut = torch.zeros(n, dtype=torch.float32, device="cuda")
-        c.lut = self.t_lut.data_ptr()
+        t = torch.zeros(n, dtype=torch.float32, device="cuda")
+        c.lut = t.data_ptr()
         _lib.check(l.sphkv_store_build_lut(ctypes.byref(c), _lib.stream_ptr()))
+        cache[key] = (t, tuple(c.lut_off), self._lut_gen())
+        self.t_lut = t
+
+    def _lut_gen(self):
+        # the tables depend only on the tier widths (eps changes do not matter)
+        return tuple((t.id, t.angle_bits) for t in self.tiers.tiers)
+
+    # Decode the 2-bit tier from per-query h-byte tables (csrc/hb_tile.cuh,
+    # exact; 3x fewer instructions per 2-bit item) instead of the quad-row
+    # table.  Off by default: measured no faster end to end on c5 (the decode
+    # is bound by per-tile latency and the P.V / V-ring pipeline, not by the
+    # 2-bit tier's instruction count -- DESIGN.md section 4).
+    hbyte_tables = False
+
+    def uses_hb(self, G):
+        """Launches with G query heads decode the 2-bit tier from per-query
+        h-byte tables (csrc/hb_tile.cuh) instead of the quad-row table."""
+        return (self.hbyte_tables and G <= 4 and self.d in (64, 128)
+                and self.page_size % 128 == 0
+                and any(t.angle_bits == 2 for t in self.tiers.non_drop))
+
+    def cptr_for(self, G):
+        """C struct for a decode launch with G query heads: selects (building
+        once) the prebuilt table variant that launch mode uses."""
+        hb = 1 if self.uses_hb(G) else 0
+        if self.cstruct.lut_flags != hb:
+            self.cstruct.lut_flags = hb
+            self._build_lut()
+        return self.cptr
 
     @property
     def cptr(self):

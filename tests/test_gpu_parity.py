@@ -312,6 +312,53 @@ def _mixed_store(sk, T, G=4, d=64, H=2, seed=3, P=128):
     return st, wl
 
 
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("G", [1, 3, 4])
+def test_two_bit_hbyte_tables_with_deaths(sk, d, G):
+    """2-bit tier through the per-query h-byte tables (G <= 4): matches the
+    oracle's recurrence, including items whose codes hit 0 or 3 (sine 0 ->
+    every later feature is 0): early deaths send the tile to the exact
+    generic path, late deaths are masked per item."""
+    rng = np.random.default_rng(d + G)
+    L, H, T, P = 1, 2, 1500, 256
+    tl = [(0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8)]
+    tiers = sk.TierTable(tuple(sk.TierSpec(*t) for t in tl))
+    keys = rng.standard_normal((L, H, T, d))
+    # deaths: a key along an axis has polar angle 0 there (code 0); a key whose
+    # tail vanishes after coordinate j has angle 0/pi at j (code 0 or 3)
+    keys[0, 0, 10, :] = 0.0
+    keys[0, 0, 10, 7] = 2.0                       # early death (row 7), tile 0
+    keys[0, 1, 700:705, d - 20:] = 0.0             # late deaths (rows ~d-21)
+    keys[0, 1, 900, d - 6:] = 0.0
+    keys[0, 1, 901, :] = -keys[0, 1, 901, :] * 0 + np.eye(d)[d - 3] * -1.5
+    r, ang = O.encode_batch(keys.reshape(-1, d))
+    r, ang = r.reshape(L, H, T), ang.reshape(L, H, T, d - 1)
+    tier = np.where(rng.random((L, H, T)) < 0.85, 1, 2).astype(np.int16)
+    z = np.ones((L, H, T), np.int8)
+    prot = np.zeros((L, H, T), bool)
+    vals = rng.standard_normal((L, H, T, d)).astype(np.float16).astype(np.float64)
+    st = sk.pack_pages_arrays(sk.TierAssignment(z, tier, prot), r, ang, vals, tiers, P)
+    assert not st.uses_hb(G)  # opt-in
+    st.hbyte_tables = True
+    assert st.uses_hb(G)
+    ost = O.pack_pages(tl, z, tier, prot, r, ang, vals, P)
+    for h in range(H):
+        q = rng.standard_normal((G, d)) * 4
+        lg, out = sk.decode.attend_heads(st, 0, h, q)
+        rq, qf = O.query_features(q)
+        for g in range(G):
+            want_lg, want_out = O.head_attend(ost, 0, h, rq[g], qf[g])
+            assert_attend_close(lg[g], out[g], want_lg, want_out)
+        # the fused launch (h-byte tables built per unit) gives the same outputs
+        import torch
+
+        qd = torch.zeros((st.groups, G, d), dtype=torch.float32, device="cuda")
+        qd[st._group(0, h)] = torch.as_tensor(q, dtype=torch.float32, device="cuda")
+        fused = sk.ada_decode(st, qd, sk.plan_store(st, groups=[st._group(0, h)], grid=3,
+                                                   units_per_cta=1))
+        assert np.max(np.abs(fused.double().cpu().numpy() - out)) <= 1e-5 * max(1, np.abs(out).max())
+
+
 def test_unit_longer_than_tile_cap(sk, monkeypatch):
     """A unit with more tiles than the kernel's tile list holds (a direct C-ABI
     caller's plan) runs as several segments with one online softmax: same
@@ -386,7 +433,7 @@ def test_page_range_split_two_level_merge(sk, world):
     for r in range(world):
         p = planmod.plan_store_range(st, groups, r, world, grid=16)
         parts = sk.decode._partials(p, G, dv)
-        _lib.check(_lib.lib().sphkv_ada_decode(st.cptr, wl.queries.data_ptr(), G,
+        _lib.check(_lib.lib().sphkv_ada_decode(st.cptr_for(G), wl.queries.data_ptr(), G,
                                                p.units.data_ptr(), p.n_units, parts.data_ptr(),
                                                None, None, p.grid, _lib.stream_ptr()))
         planmod.merge_local_state(p, parts, G, dv, gathered[r])
