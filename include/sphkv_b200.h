@@ -120,7 +120,8 @@ typedef struct {
 typedef struct {
   int32_t group;              /* (seq*layers + layer)*heads + head            */
   int32_t ptr_begin;          /* first pointer-list position                  */
-  int32_t ptr_end;            /* one past the last                            */
+  int32_t ptr_end;            /* one past the last; < 0: the list's current end
+                                 (sphkv_ada_decode_live only)                  */
   int32_t out_slot;           /* index into the partial buffer                */
 } sphkv_unit_t;
 
@@ -324,6 +325,37 @@ int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const float* q, int 
                              const int32_t* slot_group, const int32_t* slot_begin,
                              int n_groups, int32_t* ctl, float* out, int dynamic, int grid,
                              cudaStream_t stream);
+
+/* Decode-time append decision for one new key per group (decode.py:454-498):
+ * the key's radius (fp64, numpy pairwise order), its best tier
+ * (score_and_best_tier, controller.py:181-198, omega = the recent-segment
+ * weight), and with use_gate the hysteretic gate (gate.py:59-74): danger =
+ * max over the G query heads of alpha * logit_drift_bound(|q|, r_max,
+ * eps_r * r_max, eps_theta, d) / (margin + 1e-9) clamped to 10 (0 for an
+ * infinite margin), probe tier = best tier or the max tier for a drop, r_max =
+ * max page radius scale of the group; a protected head appends at the max
+ * tier with the protect flag.  keys [groups, d] (key_dtype), q fp32 [groups,
+ * G, d], margins fp32 [groups*G] (natural units, from the decode), u_hat /
+ * s_hat fp64 [groups], mode int8 [groups] gate state (0 compressible,
+ * 1 held, 2 protected; updated in place).  Outputs tier_out int16 [groups],
+ * protect_out uint8 [groups], danger_out fp32 [groups] (may be NULL). */
+int sphkv_decode_gate(const sphkv_store_t* st, const void* keys, int key_dtype, const float* q,
+                      int G, const float* margins, const double* u_hat, const double* s_hat,
+                      double r_q, double omega, double alpha_theta, double alpha_r, double lam,
+                      int use_gate, double tau_drop, double tau_prot, double gate_alpha,
+                      int8_t* mode, int16_t* tier_out, uint8_t* protect_out, float* danger_out,
+                      cudaStream_t stream);
+
+/* Decode over a store that the previous work on the stream may have grown
+ * (a decode step after an append): the fused ADA decode with the gate
+ * margins (top2/margins may both be NULL), launched without programmatic
+ * dependence, and units with ptr_end < 0 run to the group's current pointer
+ * list end, so one plan (and one captured CUDA graph) serves every step. */
+int sphkv_ada_decode_live(const sphkv_store_t* st, const float* q, int G,
+                          const sphkv_unit_t* units, int n_units, float* partials,
+                          const int32_t* slot_group, const int32_t* slot_begin, int n_groups,
+                          int32_t* ctl, float* out, float* top2, float* margins, int grid,
+                          cudaStream_t stream);
 
 /* Fused dense decode restricted to tokens >= token_begin of every planned
  * group (a sliding-window layer: the window's last W tokens only). */

@@ -6,7 +6,7 @@ schema.  Compute runs in hand-written sm_100a kernels (libsphkv_b200.so,
 C ABI in include/sphkv_b200.h); there is no CPU fallback.
 """
 
-from . import bitpack, gate, synth
+from . import bitpack, gate, rollout, synth
 from ._lib import InfeasibleProtectionError
 from .codec import (AngleCode, RadiusCode, SphericalKey, TierSpec, TierTable, angles_from_unit,
                     cos_from_angles, cos_from_codes, decode_key, encode_batch, encode_key,
@@ -20,6 +20,7 @@ from .decode import (AttentionOutput, ada_decode, angle_logits, dense_decode, de
                      logit_drift_bound, lse_merge, softmax_mix, stable_softmax)
 from .gate import GateConfig, GateState, danger_score, gate_step, margin
 from .plan import DecodePlan, plan_dense, plan_store
+from .rollout import DecodeStepper
 from .store import (DenseStore, PagedStore, ResidentBreakdown, TrafficMeter, dense_mem_estimate,
                     pack_device, pack_pages_arrays)
 

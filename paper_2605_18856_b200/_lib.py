@@ -106,11 +106,14 @@ def _declare(lib):
         "sphkv_ada_decode_margins": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, vp, vp,
                                              i, vp]),
         "sphkv_ada_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
+        "sphkv_ada_decode_live": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, vp, vp, i, vp]),
         "sphkv_dense_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
         "sphkv_dense_decode_window": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, i,
                                               vp]),
         "sphkv_partial_floats": (c_int64, [i, i]),
         "sphkv_f64_to_f16": (c_int, [vp, i64, vp, vp]),
+        "sphkv_decode_gate": (c_int, [vp, vp, i, vp, i, vp, vp, vp, d, d, d, d, d, i, d, d, d,
+                                      vp, vp, vp, vp, vp]),
         "sphkv_recon_dot": (c_int, [vp, i, i64, i, vp, i, vp, vp]),
         "sphkv_dense_logits": (c_int, [vp, vp, i64, i, vp, vp]),
         "sphkv_dense_store_logits": (c_int, [vp, vp, i, i, vp, vp]),

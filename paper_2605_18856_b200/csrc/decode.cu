@@ -113,6 +113,14 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
+// End of a unit's pointer range: ptr_end < 0 marks an open-ended unit that
+// runs to the group's CURRENT list end (a decode step attends pages the
+// previous step appended; the plan is reused unchanged, e.g. inside a CUDA
+// graph).  Such launches are not programmatic-dependent (live stores).
+__device__ __forceinline__ int unit_end(const sphkv_store_t& st, const sphkv_unit_t& u) {
+  return u.ptr_end >= 0 ? u.ptr_end : st.ptr_len[u.group];
+}
+
 // Build one segment of a unit's tile list (warp 0): whole pages of the
 // pointer range [pb, pe) in order, as many as fit in MAX_UNIT_TILES tiles.
 // Writes the tile count to seg[0] and the first pointer position NOT taken
@@ -590,7 +598,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   int u = fused_first_unit(p.fz, &s_next);
   if (u < p.n_units && warp == 0) {
     const sphkv_unit_t u0 = p.units[u];
-    build_tiles(st, u0.group, u0.ptr_begin, u0.ptr_end, 0, TI, tiles, seg, lane);
+    build_tiles(st, u0.group, u0.ptr_begin, unit_end(st, u0), 0, TI, tiles, seg, lane);
     if (lane == 0) *tile_ctr = 0;
   }
   __syncthreads();
@@ -628,6 +636,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
   const int mtn = max(0, min(mtw, MT - mt0));
   for (; u < p.n_units; first = false) {
     const sphkv_unit_t unit = p.units[u];
+    const int pe = unit_end(st, unit);  // (open-ended units: the list's current end)
     // q rows for this group, prescaled into base-2 logit units, packed pairs
     const float* qg = p.q + (size_t)unit.group * p.G * d;
     for (int i = threadIdx.x; i < d * GP; i += blockDim.x) {
@@ -660,7 +669,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
           const int pb = seg_first ? unit.ptr_begin : seg[1];
           const int ib = seg_first ? 0 : seg[2];
           __syncwarp();  // every lane has read seg[] before lane 0 rewrites it
-          build_tiles(st, unit.group, pb, unit.ptr_end, ib, TI, tiles, seg, lane);
+          build_tiles(st, unit.group, pb, pe, ib, TI, tiles, seg, lane);
           if (lane == 0) *tile_ctr = 0;
         }
         __syncthreads();
@@ -718,7 +727,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         }
         gbase += nt;
         __syncthreads();  // the tile list and seg[] may be rebuilt now
-        if (seg_end >= unit.ptr_end) break;
+        if (seg_end >= pe) break;
       }
     } else {
       // ---------------- PV warps ----------------
@@ -756,7 +765,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         }
         gbase += nt;
         __syncthreads();
-        if (seg_end >= unit.ptr_end) break;
+        if (seg_end >= pe) break;
       }
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
       pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane,
@@ -1094,7 +1103,7 @@ extern "C" int sphkv_store_build_lut(sphkv_store_t* st, cudaStream_t stream) {
 // (griddepcontrol.wait) before touching any input.
 template <typename Kern, typename Params>
 static int launch_pdl(Kern kern, const Params& p, int grid, int threads, size_t smem,
-                      cudaStream_t stream) {
+                      cudaStream_t stream, bool pdl = true) {
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3(grid);
@@ -1105,14 +1114,14 @@ static int launch_pdl(Kern kern, const Params& p, int grid, int threads, size_t 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   SPHKV_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, p));
   SPHKV_LAUNCH_CHECK();
   return SPHKV_OK;
 }
 
 template <int GP>
-static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
+static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream, bool pdl) {
   auto kern = k_ada_decode<GP>;
   cudaFuncAttributes fa;
   SPHKV_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
@@ -1123,13 +1132,13 @@ static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream) 
     return fail(SPHKV_E_UNSUPPORTED, "ADA decode needs %zu B shared memory (+%zu static) > %d",
                 smem, (size_t)fa.sharedSizeBytes, optin);
   SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream);
+  return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream, pdl);
 }
 
 static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
                            const sphkv_unit_t* units, int n_units, float* partials,
                            float* logits_dbg, const int64_t* dbg_offsets, int grid,
-                           const FusedCtl& fz, cudaStream_t stream) {
+                           const FusedCtl& fz, cudaStream_t stream, bool live = false) {
   if (!st || !q || !units || !partials) return fail(SPHKV_E_VALUE, "null argument");
   if (G < 1 || G > 8) return fail(SPHKV_E_UNSUPPORTED, "GQA group size %d outside [1, 8]", G);
   if (st->d < 3 || st->d > 256) return fail(SPHKV_E_UNSUPPORTED, "d=%d outside [3, 256]", st->d);
@@ -1192,13 +1201,13 @@ static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
   if (grid > n_units) grid = n_units;
 #ifdef SPHKV_ONLY_GP  // fast experimental builds: one GQA width only
   if (GP != SPHKV_ONLY_GP) return fail(SPHKV_E_UNSUPPORTED, "built for GP=%d only", SPHKV_ONLY_GP);
-  return launch_ada<SPHKV_ONLY_GP>(p, smem, grid, stream);
+  return launch_ada<SPHKV_ONLY_GP>(p, smem, grid, stream, !live);
 #else
   switch (GP) {
-    case 1: return launch_ada<1>(p, smem, grid, stream);
-    case 2: return launch_ada<2>(p, smem, grid, stream);
-    case 3: return launch_ada<3>(p, smem, grid, stream);
-    default: return launch_ada<4>(p, smem, grid, stream);
+    case 1: return launch_ada<1>(p, smem, grid, stream, !live);
+    case 2: return launch_ada<2>(p, smem, grid, stream, !live);
+    case 3: return launch_ada<3>(p, smem, grid, stream, !live);
+    default: return launch_ada<4>(p, smem, grid, stream, !live);
   }
 #endif
 }
@@ -1297,6 +1306,22 @@ extern "C" int sphkv_ada_decode_margins(const sphkv_store_t* st, const float* q,
   f.top2 = top2;
   f.margins = margins;
   return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream);
+}
+
+extern "C" int sphkv_ada_decode_live(const sphkv_store_t* st, const float* q, int G,
+                                     const sphkv_unit_t* units, int n_units, float* partials,
+                                     const int32_t* slot_group, const int32_t* slot_begin,
+                                     int n_groups, int32_t* ctl, float* out, float* top2,
+                                     float* margins, int grid, cudaStream_t stream) {
+  FusedCtl f;
+  int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, 0);
+  if (rc) return rc;
+  if (!slot_group) return fail(SPHKV_E_VALUE, "the live decode needs the fused merge");
+  if ((top2 == nullptr) != (margins == nullptr)) return fail(SPHKV_E_VALUE, "top2 with margins");
+  f.top2 = top2;
+  f.margins = margins;
+  return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream,
+                         true);
 }
 
 extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,

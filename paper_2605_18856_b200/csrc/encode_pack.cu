@@ -591,6 +591,83 @@ __global__ void k_score_append(const double* __restrict__ radii, int groups_per_
   if (nu_out) nu_out[i] = __ddiv_rn(__dadd_rn(d_drop, -d_best), __dadd_rn((double)rate, 1e-12));
 }
 
+// Decode-time append decision (decode.py:454-498): one warp per group.
+template <typename T>
+__global__ void k_decode_gate(sphkv_store_t st, const T* __restrict__ keys,
+                              const float* __restrict__ q, int G,
+                              const float* __restrict__ margins, const double* __restrict__ u_hat,
+                              const double* __restrict__ s_hat, double r_q, double om, double at,
+                              double ar, double lam, int use_gate, double tau_drop,
+                              double tau_prot, double galpha, int8_t* mode, int16_t* tier_out,
+                              uint8_t* prot_out, float* danger_out) {
+  const int groups = st.batch * st.layers * st.heads;
+  const int g = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (g >= groups) return;
+  const int d = st.d, NT = st.n_tiers;
+  const double sqrt_d = __dsqrt_rn((double)d);
+  // best tier of the new key (score_and_best_tier, controller.py:181-198)
+  const double radius = key_radius(keys + (int64_t)g * d, d);
+  const double w_theta =
+      __dmul_rn(__dmul_rn(__dmul_rn(at, u_hat[g]), om), __ddiv_rn(__dmul_rn(r_q, radius), sqrt_d));
+  const double w_r =
+      __dmul_rn(__dmul_rn(__dmul_rn(ar, __dadd_rn(1.0, -s_hat[g])), om), __ddiv_rn(r_q, sqrt_d));
+  int best = -1;
+  double best_s = -INFINITY;
+  for (int t = 0; t < NT; ++t) {
+    const double et = t == 0 ? 1.0 : st.tiers[t].eps_theta, er = t == 0 ? 1.0 : st.tiers[t].eps_r;
+    const double dist = __dadd_rn(__dmul_rn(w_theta, et), __dmul_rn(w_r, er));
+    const int rate = t == 0 ? 0 : (d - 1) * st.tiers[t].angle_bits + st.tiers[t].radius_bits +
+                                     st.tiers[t].meta_bits;
+    const double sc = __dadd_rn(-dist, -__dmul_rn(lam, (double)rate));
+    if (sc > best_s) {
+      best_s = sc;
+      best = t;
+    }
+  }
+  int tid = st.tiers[best].id;
+  uint8_t prot = 0;
+  float danger_f = 0.f;
+  if (use_gate) {
+    // probe tier, calibrated RMS constants (eps_r scale-relative), r_max
+    const int probe = best != 0 ? best : NT - 1;
+    const double eps_t = st.tiers[probe].eps_theta, eps_r_rel = st.tiers[probe].eps_r;
+    double r_max = 0.0;
+    const int n = st.ptr_len[g];
+    for (int i = lane; i < n; i += 32)
+      r_max = fmax(r_max, st.pages[st.ptr[(int64_t)g * st.ptr_cap + i]].radius_scale);
+    for (int o = 16; o > 0; o >>= 1) r_max = fmax(r_max, __shfl_xor_sync(0xffffffffu, r_max, o));
+    const double eps_r = __dmul_rn(eps_r_rel, r_max);
+    const double inner = __dadd_rn(__dadd_rn(__dmul_rn(r_max, eps_t), eps_r), __dmul_rn(eps_r, eps_t));
+    double danger = 0.0;
+    if (lane < G) {
+      const float* qi = q + ((int64_t)g * G + lane) * d;
+      auto sq = [qi](int i) {
+        const double v = (double)qi[i];
+        return __dmul_rn(v, v);
+      };
+      const double qn = __dsqrt_rn(np_pairwise_sum(sq, 0, d));
+      const double bound = __dmul_rn(galpha, __dmul_rn(__ddiv_rn(qn, sqrt_d), inner));
+      const double m = (double)margins[(int64_t)g * G + lane];
+      danger = isinf(m) ? 0.0 : fmin(__ddiv_rn(bound, __dadd_rn(m, 1e-9)), 10.0);
+    }
+    for (int o = 16; o > 0; o >>= 1) danger = fmax(danger, __shfl_xor_sync(0xffffffffu, danger, o));
+    int md = mode[g];
+    if (danger >= tau_prot) md = 2;
+    else if (danger <= tau_drop) md = 0;
+    if (md == 2) {
+      tid = st.tiers[NT - 1].id;
+      prot = 1;
+    }
+    if (lane == 0) mode[g] = (int8_t)md;
+    danger_f = (float)danger;
+  }
+  if (lane == 0) {
+    tier_out[g] = (int16_t)tid;
+    prot_out[g] = prot;
+    if (danger_out) danger_out[g] = danger_f;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // export: reference-format streams per page (stride = count)
 // ---------------------------------------------------------------------------
@@ -978,6 +1055,35 @@ extern "C" int sphkv_score_append(const double* radii, int groups_per_seq, int h
                                                           make_tierset(tiers_host, n_tiers),
                                                           n_tiers, lam, d, n, tier_out, score_out,
                                                           nu_out);
+  SPHKV_LAUNCH_CHECK();
+  return SPHKV_OK;
+}
+
+extern "C" int sphkv_decode_gate(const sphkv_store_t* st, const void* keys, int key_dtype,
+                                 const float* q, int G, const float* margins,
+                                 const double* u_hat, const double* s_hat, double r_q,
+                                 double omega, double alpha_theta, double alpha_r, double lam,
+                                 int use_gate, double tau_drop, double tau_prot,
+                                 double gate_alpha, int8_t* mode, int16_t* tier_out,
+                                 uint8_t* protect_out, float* danger_out, cudaStream_t stream) {
+  if (int e = validate_store(st)) return e;
+  if (!keys || !u_hat || !s_hat || !tier_out || !protect_out) return fail(SPHKV_E_VALUE, "null argument");
+  if (use_gate && (!q || !margins || !mode)) return fail(SPHKV_E_VALUE, "the gate needs q, margins, mode");
+  if (G < 1 || G > 32) return fail(SPHKV_E_UNSUPPORTED, "G=%d", G);
+  if (use_gate && !(tau_drop < tau_prot)) return fail(SPHKV_E_VALUE, "tau_drop < tau_prot");
+  if (check_dtype(key_dtype)) return SPHKV_E_VALUE;
+  const int groups = st->batch * st->layers * st->heads;
+  const int blocks = (groups * 32 + 127) / 128;
+#define SPHKV_GATE_ARGS                                                                       \
+  *st, (const T*)keys, q, G, margins, u_hat, s_hat, r_q, omega, alpha_theta, alpha_r, lam,     \
+      use_gate, tau_drop, tau_prot, gate_alpha, mode, tier_out, protect_out, danger_out
+  switch (key_dtype) {
+    case SPHKV_F32: { using T = float; k_decode_gate<T><<<blocks, 128, 0, stream>>>(SPHKV_GATE_ARGS); break; }
+    case SPHKV_F64: { using T = double; k_decode_gate<T><<<blocks, 128, 0, stream>>>(SPHKV_GATE_ARGS); break; }
+    case SPHKV_BF16: { using T = __nv_bfloat16; k_decode_gate<T><<<blocks, 128, 0, stream>>>(SPHKV_GATE_ARGS); break; }
+    default: { using T = __half; k_decode_gate<T><<<blocks, 128, 0, stream>>>(SPHKV_GATE_ARGS); break; }
+  }
+#undef SPHKV_GATE_ARGS
   SPHKV_LAUNCH_CHECK();
   return SPHKV_OK;
 }

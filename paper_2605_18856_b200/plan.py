@@ -99,7 +99,7 @@ def _page_cost(rows, d):
 
 
 def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
-               dynamic=False, tail=0.0, tail_pieces=2) -> DecodePlan:
+               dynamic=False, tail=0.0, tail_pieces=2, open_end=False) -> DecodePlan:
     """Plan a decode pass over `groups` (default: every group of the store).
 
     `tail` (with units_per_cta=1, implies dynamic): each CTA's share is cut
@@ -173,6 +173,13 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
         pieces.append([acc, int(g), rb + start, rb + len(lst)])  # (possibly empty group)
     rng = {int(g): r for g, r in zip(groups, ranges)}
     dynamic = dynamic or (tail > 0 and units_per_cta == 1)
+    if open_end:  # each group's last unit runs to the list's current end
+        last = {}
+        for pc in pieces:
+            if pc[1] not in last or pc[2] >= last[pc[1]][2]:
+                last[pc[1]] = pc
+        for pc in last.values():
+            pc[3] = -1
     return _finish(pieces, groups, grid,
                    lambda g: int(rows["count"][ptr[g, rng[g][0]:rng[g][1]]].sum()),
                    lambda g, s: int(rows["count"][ptr[g, rng[g][0]:s]].sum()) if s > rng[g][0]

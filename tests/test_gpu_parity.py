@@ -809,3 +809,114 @@ def test_errors_follow_the_reference(sk):
     with pytest.raises(ValueError):  # retained state on the drop tier
         sk.pack_pages_arrays(sk.TierAssignment(z, np.zeros((L, H, T), np.int16), prot), r, a,
                              vals, tiers, 32)
+
+
+# ---------------------------------------------------------------------------
+# decode steps with appends (decode.py:415-498)
+# ---------------------------------------------------------------------------
+
+def oracle_rollout(ost, qs, ks, vs, u_hat, s_hat, r_q, tl, eps, lam, gate_cfg, prefill, omega):
+    """Reference decode loop restated on the oracle store: per step and
+    (l, h) attention + margins, best tier of the new key, hysteretic gate,
+    append.  GQA: danger = max over the query heads.  Returns per-step
+    outputs, tiers, protect flags, modes."""
+    L, H = ost.layers, ost.heads
+    d = ost.d
+    mode = np.ones((L, H), np.int8)
+    logs = []
+    for t in range(len(qs)):
+        outs = np.zeros((L, H, qs.shape[3], ost.d_v))
+        tiers = np.zeros((L, H), np.int16)
+        prots = np.zeros((L, H), np.uint8)
+        for l in range(L):
+            for h in range(H):
+                q = qs[t, l, h]
+                rq, qf = O.query_features(q)
+                margins = []
+                for g in range(q.shape[0]):
+                    lg, out = O.head_attend(ost, l, h, rq[g], qf[g])
+                    outs[l, h, g] = out
+                    margins.append(math.inf if lg.size < 2 else float(np.diff(np.sort(lg)[-2:])[0]))
+                k = ks[t, l, h]
+                r = float(O.pairwise_norm(k[None])[0])
+                ang = O.angles_from_unit((k / (r + O.NORM_EPS))[None])[0]
+                tid = O.score_one(r, u_hat[l, h], s_hat[l, h], r_q, omega, 1.0, 1.0, tl, eps, lam,
+                                  d)[0]
+                prot = False
+                if gate_cfg is not None:
+                    probe = tid if tid != 0 else tl[-1][0]
+                    et, er_rel = eps[probe]
+                    r_max = max((ost.pages[i].scale for i in ost.pointer[(l, h)]), default=0.0)
+                    er = er_rel * r_max
+                    danger = 0.0
+                    for g in range(q.shape[0]):
+                        qn = float(O.pairwise_norm(q[g][None])[0])
+                        bound = gate_cfg.alpha * ((qn / math.sqrt(d)) * (r_max * et + er + er * et))
+                        m = margins[g]
+                        dg = 0.0 if math.isinf(m) else min(bound / (m + 1e-9), 10.0)
+                        danger = max(danger, dg)
+                    if danger >= gate_cfg.tau_prot:
+                        mode[l, h] = 2
+                    elif danger <= gate_cfg.tau_drop:
+                        mode[l, h] = 0
+                    if mode[l, h] == 2:
+                        tid, prot = tl[-1][0], True
+                tiers[l, h], prots[l, h] = tid, prot
+                ost.append_item(l, h, r, ang, vs[t, l, h], tid, prot, token_id=prefill + t)
+        logs.append((outs, tiers, prots, mode.copy()))
+    return logs
+
+
+@pytest.mark.parametrize("use_gate", [False, True])
+def test_decode_steps_with_appends_match_oracle_rollout(sk, use_gate):
+    """DecodeStepper (live decode + margins -> gate -> append, one CUDA graph
+    per step) vs the oracle restatement of the reference decode loop:
+    outputs within tolerance, per-step tier / protect / gate decisions and
+    the final SPHKV1 store bytes identical."""
+    import torch
+
+    rng = np.random.default_rng(21 + use_gate)
+    L, H, G, T, d, P, N = 2, 2, 4, 700, 64, 128, 12
+    tl = [(0, 0, 0, 0), (1, 2, 4, 8), (2, 4, 6, 8), (3, 12, 14, 8)]
+    eps = {1: (0.08, 0.02), 2: (0.02, 0.005), 3: (0.001, 0.0003)}
+    tiers = table(sk, tl, eps=[eps[1], eps[2], eps[3]])
+    keys = rng.standard_normal((L, H, T, d))
+    vals = rng.standard_normal((L, H, T, d)).astype(np.float16).astype(np.float64)
+    r, ang = O.encode_batch(keys.reshape(-1, d))
+    r, ang = r.reshape(L, H, T), ang.reshape(L, H, T, d - 1)
+    tier = rng.choice([0, 1, 2, 3], (L, H, T), p=[0.2, 0.5, 0.2, 0.1]).astype(np.int16)
+    z = (tier != 0).astype(np.int8)
+    prot = np.zeros((L, H, T), bool)
+    st = sk.pack_pages_arrays(sk.TierAssignment(z, tier, prot), r, ang, vals, tiers, P,
+                              append_tokens=64)
+    ost = O.pack_pages(tl, z, tier, prot, r, ang, vals, P)
+    u_hat = rng.uniform(0.2, 1.0, (L, H))
+    s_hat = rng.uniform(0.0, 0.8, (L, H))
+    r_q, lam, omega = 30.0, 3e-4, 1.0
+    qs = (rng.standard_normal((N, L, H, G, d)) * 3).astype(np.float32).astype(np.float64)
+    ks = rng.standard_normal((N, L, H, d))
+    ks[:, 0, 1] *= 3.0  # outlier-sized keys: page scale / new-page rule
+    ks = ks.astype(np.float32).astype(np.float64)  # the device step takes fp32 keys
+    vs = rng.standard_normal((N, L, H, d)).astype(np.float16).astype(np.float64)
+    gate_cfg = sk.GateConfig(tau_drop=0.02, tau_prot=0.2) if use_gate else None
+    want = oracle_rollout(ost, qs, ks, vs, u_hat, s_hat, r_q, tl, eps, lam, gate_cfg, T, omega)
+    stp = sk.DecodeStepper(st, G, u_hat, s_hat, r_q, lam=lam, omega=omega, gate_cfg=gate_cfg)
+    stp.capture()
+    for t in range(N):
+        out = stp.step(torch.as_tensor(qs[t].reshape(-1, G, d), dtype=torch.float32, device="cuda"),
+                       torch.as_tensor(ks[t].reshape(-1, d), dtype=torch.float32, device="cuda"),
+                       torch.as_tensor(vs[t].reshape(-1, d), dtype=torch.float16, device="cuda"),
+                       T + t)
+        w_out, w_tier, w_prot, w_mode = want[t]
+        got = out.double().cpu().numpy().reshape(L, H, G, d)
+        den = np.max(np.abs(w_out))
+        assert np.max(np.abs(got - w_out)) / den < OUT_TOL
+        assert np.array_equal(stp.tier.cpu().numpy().reshape(L, H), w_tier)
+        assert np.array_equal(stp.prot.cpu().numpy().reshape(L, H), w_prot)
+        if use_gate:
+            assert np.array_equal(stp.mode.cpu().numpy().reshape(L, H), w_mode)
+    stp.finish()
+    assert st.to_bytes() == ost.to_bytes()
+    st.check_invariants()
+    if use_gate:  # the gate must have acted somewhere for the test to mean anything
+        assert any(np.any(w[2]) for w in want) or any(np.any(w[3] == 0) for w in want)
