@@ -199,6 +199,9 @@ def build_workload(cfg_name, rank=0, world=1, mode="split", seed=0, dense=True, 
     dense_res_seq = synth.dense_resident_total(gpb, T, d, d, PAGE)
     st, ds = None, (sk.DenseStore(L, H, d, d, PAGE, batch=B) if dense else None)
     q_all = torch.zeros((B * gpb, G, d), dtype=torch.float32, device="cuda")
+    feat_u = np.zeros(B * gpb)
+    feat_s = np.zeros(B * gpb)
+    feat_rq = []
     seq_info, host_slices = [], {}
     want_slices = [s for s in PARITY_SLICES.get(cfg_name, []) if (s[0], s[2]) in pairs] \
         if parity else []
@@ -221,6 +224,9 @@ def build_workload(cfg_name, rank=0, world=1, mode="split", seed=0, dense=True, 
         u_hat, s_hat, r_q = synth.features(wl)  # normalized over this sequence's (l, h)
         torch.cuda.synchronize()
         tim["features_s"] += time.time() - t0
+        feat_u[b * gpb:(b + 1) * gpb] = u_hat
+        feat_s[b * gpb:(b + 1) * gpb] = s_hat
+        feat_rq.append(r_q)
         seg_omega = torch.as_tensor(np.asarray(synth.PANEL_OMEGA)[wl.segments], device="cuda")
         prot = torch.zeros(n, dtype=torch.uint8, device="cuda")
         t0 = time.time()
@@ -315,7 +321,8 @@ def build_workload(cfg_name, rank=0, world=1, mode="split", seed=0, dense=True, 
             "resident_dense": sum(s["resident_dense"] for s in seq_info)}
     info["resident_ratio"] = info["resident_ada"] / info["resident_dense"]
     return dict(st=st, ds=ds, q=q_all, tiers=tiers, tl=tl, info=info, timings=tim, pairs=pairs,
-                slices=host_slices)
+                slices=host_slices, u_hat=feat_u, s_hat=feat_s,
+                r_q=float(np.mean(feat_rq)) if feat_rq else 0.0)
 
 
 def time_events(fn, iters, stream):
@@ -433,6 +440,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no graphs (for ncu)")
+    ap.add_argument("--no-appends", action="store_true",
+                    help="skip the full decode steps (attention + gate + append scoring + "
+                         "append of one new key per group, rollout.DecodeStepper)")
     ap.add_argument("--hbyte", action="store_true",
                     help="2-bit tier through the per-query h-byte tables (csrc/hb_tile.cuh)")
     ap.add_argument("--units-per-cta", type=int, default=1)
@@ -725,6 +735,52 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # full decode steps with appends (decode.py:415-498): the store grows by
+    # one key per group per step, so this runs last
+    step_app = None
+    if not args.no_appends and not args.profile and mode in ("single", "shard"):
+        from paper_2605_18856_b200 import synth as synthm
+        from paper_2605_18856_b200.gate import GateConfig
+
+        nsteps = args.steps
+        gen = torch.Generator(device="cuda")
+        gen.manual_seed(4242)
+        groups = st.groups
+        kn = torch.randn((nsteps + 3, groups, d), generator=gen, device="cuda") / d ** 0.5
+        kn = (kn + torch.nn.functional.normalize(
+            torch.randn((groups, d), generator=gen, device="cuda"), dim=-1)) * 1.0
+        vn = torch.randn((nsteps + 3, groups, d), generator=gen, device="cuda").half()
+        stp = sk.DecodeStepper(st, G, W["u_hat"], W["s_hat"], W["r_q"], lam=synthm.PANEL_LAMBDA,
+                               omega=synthm.PANEL_OMEGA[2], gate_cfg=GateConfig(0.05, 0.5))
+        stp.capture(stream)
+        for t in range(3):
+            stp.step(q, kn[t], vn[t], T + t)
+        torch.cuda.synchronize()
+
+        def app_step(t):
+            stp.step(None, kn[t], vn[t], T + t)
+
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            a0.record(stream)
+            for t in range(nsteps):
+                app_step(3 + t)
+            a1.record(stream)
+        torch.cuda.synchronize()
+        app_ms = a0.elapsed_time(a1) / nsteps
+        stp.finish()
+        step_app = {"value": B / (app_ms * 1e-3), "unit": "tokens/s", "ms_per_step": app_ms,
+                    "steps": nsteps, "what": "per step: live ADA decode of every layer with "
+                    "gate margins, the decode-time gate + best-tier scoring of one new key per "
+                    "(seq, layer, kv-head), and its append (one CUDA graph)",
+                    "protected_heads_last_step": int((stp.mode == 2).sum())}
+        if world > 1:
+            t = torch.tensor([app_ms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            step_app["ms_per_step"] = float(t.item())
+            step_app["value"] = B / (step_app["ms_per_step"] * 1e-3)
+
     if rank == 0:
         ada_stream_tok = (bytes_total * (world if mode == "split" else 1)) / seqs_owned
         line = {"metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world,
@@ -753,6 +809,7 @@ def main():
                         "d2h_bytes_per_step": int(oh.numel() * 4)},
                 "gpu_launches": args.steps * (n_launch if fused else 2 * n_launch if mode != "split"
                                               else 2 * n_launch + 1),
+                "decode_step_with_appends": step_app,
                 "clocks": clk, "prefill": W["timings"], "budget": W["info"]}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -346,16 +346,20 @@ int sphkv_decode_gate(const sphkv_store_t* st, const void* keys, int key_dtype, 
                       int8_t* mode, int16_t* tier_out, uint8_t* protect_out, float* danger_out,
                       cudaStream_t stream);
 
-/* Decode over a store that the previous work on the stream may have grown
- * (a decode step after an append): the fused ADA decode with the gate
- * margins (top2/margins may both be NULL), launched without programmatic
- * dependence, and units with ptr_end < 0 run to the group's current pointer
- * list end, so one plan (and one captured CUDA graph) serves every step. */
+/* Decode over a store that decode steps grow: the fused ADA decode with the
+ * gate margins (top2/margins may both be NULL); units with ptr_end < 0 run to
+ * the group's current pointer-list end, so one plan (and one captured CUDA
+ * graph) serves every step.  flags: SPHKV_LIVE_AFTER_MUTATION -- the
+ * previous work on the stream may have changed the store (an append): no
+ * programmatic-dependent launch, the prologue may not read the page table
+ * early; SPHKV_LIVE_ABS_ROWS -- out [groups*G, d_v] and margins [groups*G]
+ * rows are indexed by absolute group id (one buffer for all layer launches). */
+enum { SPHKV_LIVE_AFTER_MUTATION = 1, SPHKV_LIVE_ABS_ROWS = 2 };
 int sphkv_ada_decode_live(const sphkv_store_t* st, const float* q, int G,
                           const sphkv_unit_t* units, int n_units, float* partials,
                           const int32_t* slot_group, const int32_t* slot_begin, int n_groups,
-                          int32_t* ctl, float* out, float* top2, float* margins, int grid,
-                          cudaStream_t stream);
+                          int32_t* ctl, float* out, float* top2, float* margins, int flags,
+                          int grid, cudaStream_t stream);
 
 /* Fused dense decode restricted to tokens >= token_begin of every planned
  * group (a sliding-window layer: the window's last W tokens only). */

@@ -25,6 +25,7 @@ SPHKV_E_CUDA = 5
 SPHKV_E_CAPACITY = 6
 
 F32, F64, BF16, F16 = 0, 1, 2, 3
+LIVE_AFTER_MUTATION, LIVE_ABS_ROWS = 1, 2
 MAX_TIERS = 16
 
 
@@ -106,7 +107,8 @@ def _declare(lib):
         "sphkv_ada_decode_margins": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, vp, vp,
                                              i, vp]),
         "sphkv_ada_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
-        "sphkv_ada_decode_live": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, vp, vp, i, vp]),
+        "sphkv_ada_decode_live": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, vp, vp, i, i,
+                                          vp]),
         "sphkv_dense_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
         "sphkv_dense_decode_window": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, i,
                                               vp]),

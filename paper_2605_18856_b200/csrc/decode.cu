@@ -65,6 +65,7 @@ struct FusedCtl {
   int dynamic;                // units claimed from ctl[n_groups] instead of u += grid
   float* top2;                // [n_slots + 1][G] second-largest logit per split, or NULL
   float* margins;             // [n_groups * G] top-1 minus top-2 logit (natural units)
+  int abs_rows;               // out / margins rows by absolute group id, not plan order
 };
 
 struct AdaParams {
@@ -397,7 +398,8 @@ __device__ __forceinline__ void pv_write(const PVState<MTW>& s, float* part, int
 // merged; the caller's loop continues with *next_unit (dynamic mode).
 __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* partials,
                                                 int out_slot, int G, int d_v, int n_units,
-                                                int* s_flag, float* s_ml, int* s_next) {
+                                                int* s_flag, float* s_ml, int* s_next,
+                                                int group = 0) {
   if (f.slot_group == nullptr && !f.dynamic) return;  // plain split partials only
   __threadfence();  // this thread's partial writes -> gpu scope before the count
   __syncthreads();
@@ -451,7 +453,8 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
       }
       if (cnt >= 2) m2 = M;
       if (lane == 0)
-        f.margins[(int64_t)gi * G + g] = (m2 == -INFINITY) ? INFINITY : (M - m2) * 0.69314718055994531f;
+        f.margins[(int64_t)(f.abs_rows ? group : gi) * G + g] =
+            (m2 == -INFINITY) ? INFINITY : (M - m2) * 0.69314718055994531f;
     }
   }
   __syncthreads();
@@ -467,7 +470,7 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
       const float v = __ldcg(partials + s * stride + 2 * G + (int64_t)g * d_v + j);
       a += (m != -INFINITY) ? v * exp2f(m - M) : 0.f;
     }
-    f.out[((int64_t)gi * G + g) * d_v + j] = (L > 0.f) ? a / L : 0.f;
+    f.out[((int64_t)(f.abs_rows ? group : gi) * G + g) * d_v + j] = (L > 0.f) ? a / L : 0.f;
   }
   if (threadIdx.x == 0) f.ctl[gi] = 0;  // every split of gi has counted: safe to re-arm
   __syncthreads();
@@ -773,7 +776,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
     }
     __syncthreads();
     fused_unit_done(p.fz, p.partials, unit.out_slot, p.G, st.d_v, p.n_units, &s_flag, s_ml,
-                    &s_next);
+                    &s_next, unit.group);
     u = p.fz.dynamic ? s_next : u + gridDim.x;
   }
   fused_kernel_exit(p.fz);
@@ -1312,7 +1315,7 @@ extern "C" int sphkv_ada_decode_live(const sphkv_store_t* st, const float* q, in
                                      const sphkv_unit_t* units, int n_units, float* partials,
                                      const int32_t* slot_group, const int32_t* slot_begin,
                                      int n_groups, int32_t* ctl, float* out, float* top2,
-                                     float* margins, int grid, cudaStream_t stream) {
+                                     float* margins, int flags, int grid, cudaStream_t stream) {
   FusedCtl f;
   int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, 0);
   if (rc) return rc;
@@ -1320,8 +1323,9 @@ extern "C" int sphkv_ada_decode_live(const sphkv_store_t* st, const float* q, in
   if ((top2 == nullptr) != (margins == nullptr)) return fail(SPHKV_E_VALUE, "top2 with margins");
   f.top2 = top2;
   f.margins = margins;
+  f.abs_rows = (flags & SPHKV_LIVE_ABS_ROWS) ? 1 : 0;
   return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream,
-                         true);
+                         (flags & SPHKV_LIVE_AFTER_MUTATION) != 0);
 }
 
 extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,

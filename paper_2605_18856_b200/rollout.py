@@ -73,13 +73,6 @@ class DecodeStepper:
                       for p in self.plans]
         self.top2 = [torch.empty((p.n_slots + 1) * G, dtype=torch.float32, device=dev)
                      for p in self.plans]
-        self.outs = [torch.empty((len(p.group_ids) * G, dv), dtype=torch.float32, device=dev)
-                     for p in self.plans]
-        self.margins_p = [torch.empty(len(p.group_ids) * G, dtype=torch.float32, device=dev)
-                          for p in self.plans]
-        self.scatter = [torch.as_tensor((np.asarray(p.group_ids)[:, None] * G
-                                         + np.arange(G)[None, :]).reshape(-1), device=dev)
-                        for p in self.plans]
         self.margins = torch.full((groups * G,), float("inf"), dtype=torch.float32, device=dev)
         self.out = torch.empty((groups, G, dv), dtype=torch.float32, device=dev)
         self.mode = torch.full((groups,), MODE_HELD, dtype=torch.int8, device=dev)
@@ -99,14 +92,15 @@ class DecodeStepper:
         l, st, G = self.l, self.st, self.G
         sp = stream.cuda_stream
         cp = st.cptr_for(G)
-        for p, part, t2, out, mg, sc in zip(self.plans, self.parts, self.top2, self.outs,
-                                            self.margins_p, self.scatter):
+        for i, (p, part, t2) in enumerate(zip(self.plans, self.parts, self.top2)):
+            # the first launch follows the previous step's append (no early
+            # page-table reads); the others overlap their predecessor (PDL)
+            flags = _lib.LIVE_ABS_ROWS | (_lib.LIVE_AFTER_MUTATION if i == 0 else 0)
             _lib.check(l.sphkv_ada_decode_live(
                 cp, self.q.data_ptr(), G, p.units.data_ptr(), p.n_units, part.data_ptr(),
                 p.slot_group.data_ptr(), p.slot_begin.data_ptr(), len(p.group_ids),
-                p.ctl.data_ptr(), out.data_ptr(), t2.data_ptr(), mg.data_ptr(), p.grid, sp))
-            self.margins.index_copy_(0, sc, mg)
-            self.out.view(-1, self.out.shape[-1]).index_copy_(0, sc, out)
+                p.ctl.data_ptr(), self.out.data_ptr(), t2.data_ptr(), self.margins.data_ptr(),
+                flags, p.grid, sp))
         g = self.gate
         _lib.check(l.sphkv_decode_gate(
             st.cptr, self.k_new.data_ptr(), _lib.F32, self.q.data_ptr(), G,
