@@ -272,6 +272,22 @@ int sphkv_export_streams(const sphkv_store_t* st, int n_pages,
 int sphkv_import_streams(const sphkv_store_t* st, int n_pages, const int64_t* offsets,
                          const uint8_t* in, cudaStream_t stream);
 
+/* ---- controller features (controller.py:99-142) --------------------------- */
+
+/* Dense prefill pass over sampled rows for every query group: keys
+ * [groups / q_per_key, tokens, d] (key_dtype; q_per_key consecutive query
+ * groups share one key group -- the G query heads of a KV head), q_rows fp64
+ * [groups, R, d] (the queries at the sampled rows), rows [R] ascending token
+ * indices.  Per group: u_raw = mean over rows
+ * of the causal softmax weight on tokens j <= row - window; inv_margin = mean
+ * over rows >= 1 of 1 / (top-1 - top-2 logit + 1e-6).  fp64 throughout.
+ * workspace: sphkv_controller_workspace_bytes(groups, R) bytes. */
+int64_t sphkv_controller_workspace_bytes(int64_t groups, int R);
+int sphkv_controller_stats(const void* keys, int key_dtype, const double* q_rows,
+                           const int32_t* rows, int R, int64_t groups, int tokens, int d,
+                           int window, int q_per_key, double* u_raw, double* inv_margin,
+                           void* workspace, cudaStream_t stream);
+
 /* ---- decode (decode.py:291-355) ------------------------------------------ */
 
 /* Tile geometry the decode kernels were built with, for the host planner:

@@ -27,6 +27,7 @@ SOURCES = {
     "rdr.cu": ["--fmad=false"],
     "recon.cu": [],
     "logits.cu": [],
+    "features.cu": [],
 }
 
 

@@ -114,6 +114,8 @@ def _declare(lib):
                                               vp]),
         "sphkv_partial_floats": (c_int64, [i, i]),
         "sphkv_f64_to_f16": (c_int, [vp, i64, vp, vp]),
+        "sphkv_controller_workspace_bytes": (c_int64, [i64, i]),
+        "sphkv_controller_stats": (c_int, [vp, i, vp, vp, i, i64, i, i, i, i, vp, vp, vp, vp]),
         "sphkv_decode_gate": (c_int, [vp, vp, i, vp, i, vp, vp, vp, d, d, d, d, d, i, d, d, d,
                                       vp, vp, vp, vp, vp]),
         "sphkv_recon_dot": (c_int, [vp, i, i64, i, vp, i, vp, vp]),

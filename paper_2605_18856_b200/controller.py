@@ -7,8 +7,8 @@ variants (`*_device`) serve the batched prefill path; the numpy-shaped
 functions keep the reference signatures.
 
 compute_features (controller.py:99-142) is an input contract of the hot
-path; it is evaluated here with fp64 tensor math on the
-GPU and will move to a dedicated kernel.
+path; its masked prefill pass is the fp64
+sphkv_controller_stats kernel (csrc/features.cu).
 """
 
 from __future__ import annotations
@@ -301,47 +301,72 @@ def downtier_before_drop(initial: TierAssignment, scores: StateScores, budget_bi
 # features (input contract)
 # ---------------------------------------------------------------------------
 
-def compute_features(workload, config: ControllerConfig, max_rows: int = MAX_FEATURE_ROWS):
-    """Head reuse / stability scalars from a dense prefill pass (controller.py:99-142),
-    evaluated with fp64 tensor math on the GPU."""
+def feature_rows(T: int, max_rows: int = MAX_FEATURE_ROWS) -> np.ndarray:
+    """Sampled prefill rows (controller.py:108-111)."""
+    if T <= max_rows:
+        return np.arange(T)
+    return np.unique(np.round(np.linspace(0, T - 1, max_rows)).astype(int))
+
+
+def controller_stats_device(keys, q_rows, rows, window):
+    """u_raw, inv_margin per query group on the device (sphkv_controller_stats):
+    keys [kv_groups, T, d] (bf16/fp16/fp32/fp64 tensor), q_rows fp64
+    [kv_groups * q_per_key, R, d] device tensor (the q_per_key query rows of a
+    KV group consecutive), rows [R] sampled token indices."""
     import torch
 
-    keys = torch.as_tensor(np.asarray(workload.keys), dtype=torch.float64, device="cuda")
-    queries = torch.as_tensor(np.asarray(workload.queries), dtype=torch.float64, device="cuda")
+    l = _lib.require_gpu()
+    kv_groups, T, d = keys.shape
+    groups = q_rows.shape[0]
+    R = len(rows)
+    kd = {torch.float32: _lib.F32, torch.float64: _lib.F64, torch.bfloat16: _lib.BF16,
+          torch.float16: _lib.F16}[keys.dtype]
+    keys = keys.contiguous()
+    q_rows = q_rows.to(device="cuda", dtype=torch.float64).contiguous()
+    rows_t = torch.as_tensor(np.asarray(rows, dtype=np.int32), device="cuda")
+    u = torch.empty(groups, dtype=torch.float64, device="cuda")
+    m = torch.empty(groups, dtype=torch.float64, device="cuda")
+    ws = torch.empty(l.sphkv_controller_workspace_bytes(groups, R), dtype=torch.uint8,
+                     device="cuda")
+    _lib.check(l.sphkv_controller_stats(keys.data_ptr(), kd, q_rows.data_ptr(),
+                                        rows_t.data_ptr(), R, groups, T, d, int(window),
+                                        groups // kv_groups, u.data_ptr(), m.data_ptr(),
+                                        ws.data_ptr(), _lib.stream_ptr()))
+    return u, m
+
+
+def normalize_features(u_raw, inv_margin):
+    """Across-head normalization (controller.py:135-140) of host arrays."""
+    u_raw, inv_margin = np.asarray(u_raw, np.float64), np.asarray(inv_margin, np.float64)
+    u_max = u_raw.max()
+    u_hat = u_raw / u_max if u_max > 0 else np.ones_like(u_raw)
+    m_max = inv_margin.max()
+    s_hat = 1.0 - (inv_margin / m_max if m_max > 0 else np.zeros_like(inv_margin))
+    return u_hat, s_hat
+
+
+def compute_features(workload, config: ControllerConfig, max_rows: int = MAX_FEATURE_ROWS):
+    """Head reuse / stability scalars from a dense prefill pass (controller.py:99-142):
+    the masked softmax / top-2 pass over the sampled rows runs in the fp64
+    sphkv_controller_stats kernel; the normalization across heads and r_q
+    are host reductions."""
+    import torch
+
+    keys = np.asarray(workload.keys)
+    queries = np.asarray(workload.queries)
     L, H, T, d = keys.shape
     if T == 0:
         raise ValueError("empty prefill")
     window = max(T // 8, 1)
-    if T <= max_rows:
-        rows = np.arange(T)
-    else:
-        rows = np.unique(np.round(np.linspace(0, T - 1, max_rows)).astype(int))
-    rows_t = torch.as_tensor(rows, device="cuda")
-    ar = torch.arange(T, device="cuda")
-    mask = ar[None, :] > rows_t[:, None]
-    old = ar[None, :] <= (rows_t[:, None] - window)
-    ok = rows_t >= 1
-    u_raw = torch.zeros((L, H), dtype=torch.float64, device="cuda")
-    inv_margin = torch.zeros((L, H), dtype=torch.float64, device="cuda")
-    scale = math.sqrt(d)
-    for l in range(L):
-        q = queries[l][:, rows_t]                       # (H, R, d)
-        logits = torch.einsum("hrd,htd->hrt", q, keys[l]) / scale
-        logits = logits.masked_fill(mask[None], -math.inf)
-        w = torch.softmax(logits, dim=-1)
-        u_raw[l] = torch.where(old[None], w, 0.0).sum(-1).mean(-1)
-        if bool(ok.any()):
-            top2 = torch.topk(logits[:, ok], 2, dim=-1).values
-            inv_margin[l] = (1.0 / (top2[..., 0] - top2[..., 1] + _MARGIN_EPS)).mean(-1)
-    u_max = float(u_raw.max())
-    u_hat = (u_raw / u_max) if u_max > 0 else torch.ones_like(u_raw)
-    m_max = float(inv_margin.max())
-    s_hat = 1.0 - ((inv_margin / m_max) if m_max > 0 else torch.zeros_like(inv_margin))
-    r_q = float(torch.linalg.norm(queries, dim=-1).mean())
-    return ControllerFeatures(u_hat=u_hat.cpu().numpy(), s_hat=s_hat.cpu().numpy(), r_q=r_q,
-                              omega=config.omega, alpha_theta=config.alpha_theta,
-                              alpha_r=config.alpha_r, segments=np.asarray(workload.segments),
-                              prefill=T)
+    rows = feature_rows(T, max_rows)
+    kd = torch.as_tensor(keys.reshape(L * H, T, d), dtype=torch.float64, device="cuda")
+    qd = torch.as_tensor(queries.reshape(L * H, T, d)[:, rows], dtype=torch.float64, device="cuda")
+    u, m = controller_stats_device(kd, qd, rows, window)
+    u_hat, s_hat = normalize_features(u.cpu().numpy().reshape(L, H), m.cpu().numpy().reshape(L, H))
+    r_q = float(np.mean(np.linalg.norm(queries, axis=-1)))
+    return ControllerFeatures(u_hat=u_hat, s_hat=s_hat, r_q=r_q, omega=config.omega,
+                              alpha_theta=config.alpha_theta, alpha_r=config.alpha_r,
+                              segments=np.asarray(workload.segments), prefill=T)
 
 
 def protected_mask(workload, config: ControllerConfig) -> np.ndarray:

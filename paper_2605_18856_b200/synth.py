@@ -94,43 +94,37 @@ def generate(batch, layers, heads, G, tokens, d, d_v=None, seed=0, chunk_groups=
 
 def features(wl: Workload, rows=512, seed=1):
     """u_hat / s_hat / r_q per (seq, layer, kv-head) from a sampled dense prefill
-    pass (controller.py:99-142 recipe; GQA: the G query heads' sampled rows of
-    a KV head are pooled).  Returns fp64 numpy (B*L*H,), (B*L*H,), float."""
+    pass (controller.py:99-142 recipe, the fp64 sphkv_controller_stats kernel;
+    GQA: the G query heads' sampled rows of a KV head are pooled).  The prefill
+    queries at the sampled rows are drawn from the workload's query
+    distribution.  Returns fp64 numpy (B*L*H,), (B*L*H,), float."""
     import torch
+    from .controller import controller_stats_device, feature_rows, normalize_features
 
-    T, d = wl.tokens, wl.d
+    T, d, G = wl.tokens, wl.d, wl.G
     gen = torch.Generator(device="cuda")
     gen.manual_seed(seed)
     window = max(T // 8, 1)
-    r_idx = torch.as_tensor(np.unique(np.round(np.linspace(0, T - 1, min(rows, T))).astype(int)),
-                            device="cuda")
-    R = r_idx.numel()
-    ar = torch.arange(T, device="cuda")
-    mask = ar[None, :] > r_idx[:, None]
-    old = ar[None, :] <= (r_idx[:, None] - window)
-    ok = r_idx >= 1
-    u_raw = torch.zeros(wl.groups, dtype=torch.float64, device="cuda")
-    inv_m = torch.zeros(wl.groups, dtype=torch.float64, device="cuda")
-    sd = 1.0 / math.sqrt(d)
+    r_idx = feature_rows(T, rows)
+    R = len(r_idx)
+    u_raw = np.zeros(wl.groups)
+    inv_m = np.zeros(wl.groups)
     qnorms = []
-    for g in range(wl.groups):
-        tp = wl.topic[g].double()
-        qn = torch.randn((wl.G, R, d), generator=gen, device="cuda", dtype=torch.float64) * sd
-        qd = tp + 0.5 * qn
-        qd = qd / qd.norm(dim=-1, keepdim=True)
-        q = qd * (4.0 * math.sqrt(d))
-        qnorms.append(q.norm(dim=-1).mean())
-        k = wl.keys[g].double()
-        lg = torch.einsum("grd,td->grt", q, k) * sd
-        lg = lg.masked_fill(mask[None], -math.inf)
-        w = torch.softmax(lg, dim=-1)
-        u_raw[g] = torch.where(old[None], w, 0.0).sum(-1).mean()
-        top2 = torch.topk(lg[:, ok], 2, dim=-1).values
-        inv_m[g] = (1.0 / (top2[..., 0] - top2[..., 1] + 1e-6)).mean()
-    u_hat = u_raw / u_raw.max() if float(u_raw.max()) > 0 else torch.ones_like(u_raw)
-    s_hat = 1.0 - (inv_m / inv_m.max() if float(inv_m.max()) > 0 else torch.zeros_like(inv_m))
-    r_q = float(torch.stack(qnorms).mean())
-    return u_hat.cpu().numpy(), s_hat.cpu().numpy(), r_q
+    chunk = 64
+    for g0 in range(0, wl.groups, chunk):
+        g1 = min(wl.groups, g0 + chunk)
+        tp = wl.topic[g0:g1].double()
+        qn = torch.randn((g1 - g0, G, R, d), generator=gen, device="cuda",
+                         dtype=torch.float64) / math.sqrt(d)
+        qd = tp[:, None, None, :] + 0.5 * qn
+        q = qd / qd.norm(dim=-1, keepdim=True) * (4.0 * math.sqrt(d))
+        qnorms.append(q.norm(dim=-1).mean(dim=(1, 2)))
+        u, m = controller_stats_device(wl.keys[g0:g1], q.reshape(-1, R, d), r_idx, window)
+        u_raw[g0:g1] = u.view(-1, G).mean(-1).cpu().numpy()
+        inv_m[g0:g1] = m.view(-1, G).mean(-1).cpu().numpy()
+    u_hat, s_hat = normalize_features(u_raw, inv_m)
+    r_q = float(torch.cat(qnorms).mean())
+    return u_hat, s_hat, r_q
 
 
 def panel_tiers(eps=None, d=128, sample_keys=None, seed=0):
