@@ -661,22 +661,24 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       }
     }
 #endif
-    // A unit runs as one or more segments of <= MAX_UNIT_TILES tiles.  The
-    // logit and PV warps run their own segment loops (separate register
-    // sets: the PV warps' online-softmax state lives only in theirs) that meet
-    // at the same two block barriers per segment.
-    if (warp < ADA_NL) {
-      // ---------------- logit warps ----------------
-      for (bool seg_first = true;; seg_first = false) {
-        if (!(first && seg_first) && warp == 0) {
-          const int pb = seg_first ? unit.ptr_begin : seg[1];
-          const int ib = seg_first ? 0 : seg[2];
-          __syncwarp();  // every lane has read seg[] before lane 0 rewrites it
-          build_tiles(st, unit.group, pb, pe, ib, TI, tiles, seg, lane);
-          if (lane == 0) *tile_ctr = 0;
-        }
-        __syncthreads();
-        const int nt = seg[0], seg_end = seg[1];  // read before warp 0 may rebuild
+    // A unit runs as one or more segments of <= MAX_UNIT_TILES tiles; the
+    // online-softmax state of the PV warps carries across segments.  Every
+    // warp runs the same loop and meets the same block barriers.
+    PVState<ADA_MTW> s;
+    if (warp >= ADA_NL) pv_init(s);
+    const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
+    for (bool seg_first = true;; seg_first = false) {
+      if (!(first && seg_first) && warp == 0) {
+        const int pb = seg_first ? unit.ptr_begin : seg[1];
+        const int ib = seg_first ? 0 : seg[2];
+        __syncwarp();  // every lane has read seg[] before lane 0 rewrites it
+        build_tiles(st, unit.group, pb, pe, ib, TI, tiles, seg, lane);
+        if (lane == 0) *tile_ctr = 0;
+      }
+      __syncthreads();
+      const int nt = seg[0], seg_end = seg[1];  // read before warp 0 may rebuild
+      if (warp < ADA_NL) {
+        // ---------------- logit warps ----------------
         if (!lut_ready) {
           ptx::mbar_wait(lut_bar, 0);
           lut_ready = true;
@@ -728,21 +730,11 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
         }
-        gbase += nt;
-        __syncthreads();  // the tile list and seg[] may be rebuilt now
-        if (seg_end >= pe) break;
-      }
-    } else {
-      // ---------------- PV warps ----------------
-      // NPV warps split the d_v m-tiles; all consume every tile in order.
-      // Lane 0 of PV warp 0 is also the V producer: it refills slot vs once
-      // every PV warp has released it (v_empty counts NPV arrivals).
-      PVState<ADA_MTW> s;
-      pv_init(s);
-      const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
-      for (bool seg_first = true;; seg_first = false) {
-        __syncthreads();
-        const int nt = seg[0], seg_end = seg[1];
+      } else {
+        // ---------------- PV warps ----------------
+        // NPV warps split the d_v m-tiles; all consume every tile in order.
+        // Lane 0 of PV warp 0 is also the V producer: it refills slot vs once
+        // every PV warp has released it (v_empty counts NPV arrivals).
         if (!(first && seg_first) && pw == 0 && lane == 0)
           for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k, gbase);
         for (int k = 0; k < nt; ++k) {
@@ -766,10 +758,12 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
             if (pw == 0 && k + ADA_NV < nt) issue_v(k + ADA_NV, gbase);
           }
         }
-        gbase += nt;
-        __syncthreads();
-        if (seg_end >= pe) break;
       }
+      gbase += nt;
+      __syncthreads();  // the tile list and seg[] may be rebuilt now
+      if (seg_end >= pe) break;
+    }
+    if (warp >= ADA_NL) {
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
       pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane,
                         p.fz.top2 != nullptr ? p.fz.top2 + (size_t)unit.out_slot * p.G : nullptr);
