@@ -579,10 +579,24 @@ def main():
         gathered = torch.empty((world, n_launch, ng, F), dtype=torch.float32, device="cuda")
         out_all = torch.empty((n_launch * ng * G, d), dtype=torch.float32, device="cuda")
 
-        def step_fn():
-            decode_layers(with_merge=False)
+        def local_layers():  # each rank's share: one fused launch per layer -> states
             for l, p in enumerate(plans):
-                planmod.merge_local_state(p, parts[l], G, d, state[l], stream)
+                _lib.check(lib.sphkv_ada_decode_state(
+                    st.cptr_for(G), q.data_ptr(), G, p.units.data_ptr(), p.n_units,
+                    parts[l].data_ptr(), p.slot_group.data_ptr(), p.slot_begin.data_ptr(), ng,
+                    p.ctl.data_ptr(), state[l].data_ptr(), p.grid, sp))
+
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                local_layers()
+        torch.cuda.synchronize()
+        lgraph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(lgraph, stream=stream):
+            local_layers()
+
+        def step_fn():
+            with torch.cuda.stream(stream):
+                lgraph.replay()
             with torch.cuda.stream(stream):
                 if gloo_dbg:
                     g_h = torch.empty(gathered.numel(), dtype=torch.float32)
@@ -808,7 +822,7 @@ def main():
                         "h2d_bytes_per_step": int(qh.numel() * 4),
                         "d2h_bytes_per_step": int(oh.numel() * 4)},
                 "gpu_launches": args.steps * (n_launch if fused else 2 * n_launch if mode != "split"
-                                              else 2 * n_launch + 1),
+                                              else n_launch + 1),
                 "decode_step_with_appends": step_app,
                 "clocks": clk, "prefill": W["timings"], "budget": W["info"]}
         print(json.dumps(line), flush=True)

@@ -342,6 +342,16 @@ int sphkv_dense_decode_fused(const sphkv_dense_store_t* st, const float* q, int 
                              int n_groups, int32_t* ctl, float* out, int dynamic, int grid,
                              cudaStream_t stream);
 
+/* Fused ADA decode whose in-kernel merge writes each planned group's STATE
+ * (one partial slot [G*(d_v+2)] per group: m = log2-sum-exp, l = 1, acc =
+ * normalized output; all-empty: -inf, 0, 0) instead of output rows -- a
+ * rank's page-range share in one launch, ready for the all-gather and
+ * sphkv_lse_merge_ex over ranks. */
+int sphkv_ada_decode_state(const sphkv_store_t* st, const float* q, int G,
+                           const sphkv_unit_t* units, int n_units, float* partials,
+                           const int32_t* slot_group, const int32_t* slot_begin, int n_groups,
+                           int32_t* ctl, float* state_out, int grid, cudaStream_t stream);
+
 /* Decode-time append decision for one new key per group (decode.py:454-498):
  * the key's radius (fp64, numpy pairwise order), its best tier
  * (score_and_best_tier, controller.py:181-198, omega = the recent-segment

@@ -107,6 +107,7 @@ def _declare(lib):
         "sphkv_ada_decode_margins": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, vp, vp,
                                              i, vp]),
         "sphkv_ada_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),
+        "sphkv_ada_decode_state": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, vp]),
         "sphkv_ada_decode_live": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, vp, vp, i, i,
                                           vp]),
         "sphkv_dense_decode_fused": (c_int, [vp, vp, i, vp, i, vp, vp, vp, i, vp, vp, i, i, vp]),

@@ -66,6 +66,9 @@ struct FusedCtl {
   float* top2;                // [n_slots + 1][G] second-largest logit per split, or NULL
   float* margins;             // [n_groups * G] top-1 minus top-2 logit (natural units)
   int abs_rows;               // out / margins rows by absolute group id, not plan order
+  int state_out;              // out = one partial-state slot per group (m = log2-sum-exp,
+                              // l = 1, acc = normalized output): a page-range split's
+                              // local result, ready for the all-gather and merge over ranks
 };
 
 struct AdaParams {
@@ -470,7 +473,15 @@ __device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* 
       const float v = __ldcg(partials + s * stride + 2 * G + (int64_t)g * d_v + j);
       a += (m != -INFINITY) ? v * exp2f(m - M) : 0.f;
     }
-    f.out[((int64_t)(f.abs_rows ? group : gi) * G + g) * d_v + j] = (L > 0.f) ? a / L : 0.f;
+    if (f.state_out)
+      f.out[(int64_t)gi * stride + 2 * G + (int64_t)g * d_v + j] = (L > 0.f) ? a / L : 0.f;
+    else
+      f.out[((int64_t)(f.abs_rows ? group : gi) * G + g) * d_v + j] = (L > 0.f) ? a / L : 0.f;
+  }
+  if (f.state_out && threadIdx.x < G) {  // (m, l) of the state slot (k_lse_merge state_out)
+    const float M = s_ml[threadIdx.x], L = s_ml[8 + threadIdx.x];
+    f.out[(int64_t)gi * stride + threadIdx.x] = (L > 0.f) ? M + log2f(L) : -INFINITY;
+    f.out[(int64_t)gi * stride + G + threadIdx.x] = (L > 0.f) ? 1.f : 0.f;
   }
   if (threadIdx.x == 0) f.ctl[gi] = 0;  // every split of gi has counted: safe to re-arm
   __syncthreads();
@@ -1320,6 +1331,19 @@ extern "C" int sphkv_ada_decode_live(const sphkv_store_t* st, const float* q, in
   f.abs_rows = (flags & SPHKV_LIVE_ABS_ROWS) ? 1 : 0;
   return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream,
                          (flags & SPHKV_LIVE_AFTER_MUTATION) != 0);
+}
+
+extern "C" int sphkv_ada_decode_state(const sphkv_store_t* st, const float* q, int G,
+                                      const sphkv_unit_t* units, int n_units, float* partials,
+                                      const int32_t* slot_group, const int32_t* slot_begin,
+                                      int n_groups, int32_t* ctl, float* state_out, int grid,
+                                      cudaStream_t stream) {
+  FusedCtl f;
+  int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, state_out, 0);
+  if (rc) return rc;
+  if (!slot_group) return fail(SPHKV_E_VALUE, "the state output needs the fused merge");
+  f.state_out = 1;
+  return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream);
 }
 
 extern "C" int sphkv_dense_decode(const sphkv_dense_store_t* st, const float* q, int G,

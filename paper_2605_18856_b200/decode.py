@@ -86,6 +86,27 @@ def ada_decode(store, q, plan: DecodePlan | None = None, *, out=None, partials=N
     return out
 
 
+def ada_decode_state(store, q, plan: DecodePlan, *, state=None, partials=None, stream=None):
+    """Fused decode of a (rank's page-range) plan whose in-kernel merge emits
+    one partial STATE per planned group ([len(plan.group_ids), G*(d_v+2)]:
+    log2-sum-exp, 1, normalized output) -- the operand of the all-gather and
+    merge over ranks (plan.merge_gathered)."""
+    import torch
+
+    l = _lib.require_gpu()
+    G = q.shape[-2]
+    ng = len(plan.group_ids)
+    if partials is None:
+        partials = _partials(plan, G, store.d_v)
+    if state is None:
+        state = torch.empty((ng, G * (store.d_v + 2)), dtype=torch.float32, device="cuda")
+    _lib.check(l.sphkv_ada_decode_state(
+        store.cptr_for(G), q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
+        partials.data_ptr(), plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng,
+        plan.ctl.data_ptr(), state.data_ptr(), plan.grid, _lib.stream_ptr(stream)))
+    return state
+
+
 def dense_decode(dstore, q, plan: DecodePlan | None = None, *, out=None, partials=None,
                  stream=None, token_begin=0):
     """Dense bf16 paged decode (decode.py:63-69, 302-307); `token_begin` > 0

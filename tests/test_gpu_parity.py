@@ -437,6 +437,10 @@ def test_page_range_split_two_level_merge(sk, world):
                                                p.units.data_ptr(), p.n_units, parts.data_ptr(),
                                                None, None, p.grid, _lib.stream_ptr()))
         planmod.merge_local_state(p, parts, G, dv, gathered[r])
+        # the fused single-launch form (in-kernel merge emits the rank's state)
+        fused = sk.decode.ada_decode_state(st, wl.queries, p)
+        assert torch.allclose(fused, gathered[r], rtol=2e-5, atol=2e-5)
+        gathered[r] = fused
     out = torch.empty_like(want)
     planmod.merge_gathered(len(groups), world, gathered, G, dv, out)
     assert torch.allclose(out, want, rtol=2e-5, atol=2e-5)

@@ -145,3 +145,143 @@ def test_gloo_world2_page_range_split(tmp_path):
         rq, qf = O.query_features(q[l, h][None])
         _, want = O.head_attend(st, l, h, rq[0], qf[0])
         assert np.max(np.abs(got[gi] - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+
+
+# ---------------------------------------------------------------------------
+# batch x KV-head shards: ownership and per-sequence RDR
+# ---------------------------------------------------------------------------
+
+def test_shard_ownership_covers_every_pair_once():
+    import bench
+
+    for B, H in ((16, 8), (8, 8), (4, 8), (1, 8), (3, 5)):
+        for world in (1, 2, 3, 4, 8):
+            owned = [bench.owned_pairs(B, H, r, world, "shard") for r in range(world)]
+            flat = [p for o in owned for p in o]
+            assert sorted(flat) == [(b, h) for b in range(B) for h in range(H)]
+            for o in owned:  # a rank's heads of one sequence are a contiguous range
+                for b in {p[0] for p in o}:
+                    hs = sorted(h for bb, h in o if bb == b)
+                    assert hs == list(range(hs[0], hs[-1] + 1))
+
+
+def _alloc_worker(rank, world, port, result_path):
+    """Each rank holding part of sequence 0 runs the SAME per-sequence RDR
+    allocation (oracle score + greedy, controller.py:213-346) on the whole
+    sequence and keeps its own heads; the gathered decisions must agree."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(11)  # the sequence's data: identical on every rank
+    L, H, T, d = 2, 4, 300, 16
+    radii = np.abs(rng.standard_normal((L, H, T))) + 0.5
+    eps = {1: (0.08, 0.02), 2: (0.02, 0.005), 3: (0.001, 0.0003)}
+    seg = np.full(T, 2, np.int8)
+    seg[:200] = 0
+    prot = np.zeros((L, H, T), bool)
+    sc = O.score_states(radii, rng.uniform(0.2, 1, (L, H)), rng.uniform(0, 0.8, (L, H)), 30.0,
+                        (0.02, 2.0, 1.0), seg, 1.0, 1.0, TIERS, eps, 3e-5, prot, d)
+    z, tier = O.allocate_greedy(sc["best_tier"], sc["nu"], prot, int(0.3 * L * H * T * d * 16),
+                                TIERS, d)
+    t = torch.from_numpy(tier.astype(np.int64).reshape(-1))
+    g = torch.empty(world * t.numel(), dtype=t.dtype)
+    dist.all_gather_into_tensor(g, t)
+    if rank == 0:
+        np.save(result_path, g.numpy().reshape(world, -1))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_replicated_sequence_allocation(tmp_path):
+    import torch.multiprocessing as mp
+
+    res = str(tmp_path / "alloc.npy")
+    mp.spawn(_alloc_worker, args=(2, _free_port(), res), nprocs=2, join=True)
+    got = np.load(res)
+    assert np.array_equal(got[0], got[1]) and np.any(got[0] == 0) and np.any(got[0] > 0)
+
+
+def _device_worker(rank, world, port, result_path):
+    """Both ranks on cuda:0 over gloo: device page-range decode of the rank's
+    share (fused state output), all-gather of the states, device merge."""
+    import torch
+    import torch.distributed as dist
+    import paper_2605_18856_b200 as sk
+    from paper_2605_18856_b200 import plan as planmod
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    st, q, tl = _device_store(sk)
+    groups = list(range(st.groups))
+    p = planmod.plan_store_range(st, groups, rank, world, grid=16)
+    state = sk.decode.ada_decode_state(st, q, p).cpu()
+    gathered = torch.empty((world,) + tuple(state.shape), dtype=state.dtype)
+    dist.all_gather_into_tensor(gathered.view(-1), state.view(-1))
+    G, dv = q.shape[1], st.d_v
+    out = torch.empty((len(groups) * G, dv), dtype=torch.float32, device="cuda")
+    planmod.merge_gathered(len(groups), world, gathered.cuda(), G, dv, out)
+    if rank == 0:
+        np.save(result_path, out.double().cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _device_store(sk):
+    import torch
+
+    rng = np.random.default_rng(5)
+    L, H, T, d, G, P = 2, 2, 2500, 64, 4, 128
+    keys = rng.standard_normal((L, H, T, d))
+    vals = rng.standard_normal((L, H, T, d)).astype(np.float16).astype(np.float64)
+    r, ang = O.encode_batch(keys.reshape(-1, d))
+    tier = rng.choice([0, 1, 2, 3], (L, H, T), p=[0.1, 0.4, 0.3, 0.2]).astype(np.int16)
+    tiers = sk.TierTable(tuple(sk.TierSpec(*t) for t in TIERS))
+    st = sk.pack_pages_arrays(sk.TierAssignment((tier != 0).astype(np.int8), tier,
+                                                np.zeros((L, H, T), bool)),
+                              r.reshape(L, H, T), ang.reshape(L, H, T, d - 1), vals, tiers, P)
+    q = torch.as_tensor(rng.standard_normal((L * H, G, d)) * 4, dtype=torch.float32,
+                        device="cuda")
+    return st, q, TIERS
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(600)
+def test_gloo_world2_device_page_range_split(tmp_path):
+    """The N > 1 page-range data path through the DEVICE kernels: two gloo
+    ranks (both on the one GPU) decode their shares, all-gather the states and
+    merge; equals the single-pass device decode and the oracle."""
+    import torch
+    import torch.multiprocessing as mp
+    import paper_2605_18856_b200 as sk
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    res = str(tmp_path / "dev.npy")
+    ctx = mp.get_context("spawn")
+    procs = [ctx.Process(target=_device_worker, args=(r, 2, _free_port_shared(), res))
+             for r in range(2)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(timeout=500)
+        assert pr.exitcode == 0
+    got = np.load(res)
+    st, q, _ = _device_store(sk)
+    want = sk.ada_decode(st, q, sk.plan_store(st)).double().cpu().numpy()
+    assert np.max(np.abs(got - want)) <= 2e-5 * max(1.0, np.abs(want).max())
+
+
+_PORT = None
+
+
+def _free_port_shared():
+    global _PORT
+    if _PORT is None:
+        _PORT = _free_port()
+    return _PORT
