@@ -7,19 +7,25 @@
 //   decode.py:63-69, 302-307  dense path (DenseStore)
 //   decode.py:347-354  one softmax over all logits  ->  split partials + LSE
 //
-// ADA kernel (one persistent CTA per SM, ~210 KB smem):
-//   warps 0..NL-1  logit warps: a 128-item tile per warp, 4 items per lane.
-//                  Angle codes are read straight from the page's coordinate-
-//                  major rows (L2-prefetched by cp.async.bulk.prefetch),
-//                  (cos, sin) of polar codes come from a shared-memory LUT,
-//                  the feature recurrence runs in fp32 registers and the G
-//                  query heads are dotted with packed FFMA2.  Tile max/sum
-//                  and fp16 weights go to a P slot.
+// ADA kernel (one persistent CTA per SM, ~210 KB smem, one launch per layer):
+//   warps 0..NL-1  logit warps: a 128-item tile per warp, 4 items per lane,
+//                  claimed dynamically inside the CTA.  Each lane loads its
+//                  items' code strings from the page's word-interleaved
+//                  block (L2-prefetched PF_DIST tiles ahead by
+//                  cp.async.bulk.prefetch), looks (cos, sin) -- or products of
+//                  four rows' factors -- up in shared-memory tables, runs the
+//                  feature recurrence in fp32 registers and dots the G query
+//                  heads with packed FFMA2 (the 2-bit tier optionally through
+//                  per-query h-byte tables, hb_tile.cuh).  Tile max/sum and
+//                  fp16 weights go to a P slot (12-slot ring).
 //   warp NL        PV warp: V^T (ldmatrix.trans of the TMA-staged, swizzled
 //                  fp16 V tile) x P (fp16) on mma.sync, fp32 accumulate,
 //                  online-softmax combine across tiles, writes the partial.
 //                  Lane 0 also issues the 1-D TMA bulk copies of V tiles into a
-//                  4-slot ring (evict_first), NV tiles ahead of consumption.
+//                  2-slot ring (evict_first), NV tiles ahead of consumption.
+//   The CTA finishing a group's last split merges the group's partials
+//   (fused LSE merge) into output rows, a partial state (page-range split),
+//   and the gate margins when asked.
 #include "common.cuh"
 #include "ptx.cuh"
 #include "ada_tile.cuh"

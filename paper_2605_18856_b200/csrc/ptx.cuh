@@ -68,11 +68,6 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gmem, uint32_t bytes,
                                               uint64_t* bar, uint64_t policy) {
   asm volatile(
@@ -81,19 +76,11 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gm
       ::"r"(smem_u32(dst_smem)), "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void bulk_prefetch_l2_hint(const void* src, uint32_t bytes,
-                                                      uint64_t policy) {
-  asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;"
-               ::"l"(src), "r"(bytes), "l"(policy) : "memory");
-}
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void prefetch_l1_line(const void* p) {
   asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
-__device__ __forceinline__ void prefetch_l2_line(const void* p) {
-  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
 }
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -159,21 +146,11 @@ __device__ __forceinline__ float f2_lo(f2 x) {
 __device__ __forceinline__ float f2_hi(f2 x) {
   return __uint_as_float((uint32_t)(x.v >> 32));
 }
-// acc + (s, s) * q  -- SASS folds the broadcast into FFMA2 Rs.F32
-__device__ __forceinline__ f2 f2_fma_s(float s, f2 q, f2 acc) {
-  f2 r;
-  f2 ss = f2_make(s, s);
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(ss.v), "l"(q.v), "l"(acc.v));
-  return r;
-}
 // in-place accumulate (tied operand): keeps loop-carried accumulators in
 // fixed registers so unrolled loops need no copy-back moves
 __device__ __forceinline__ void f2_fma_s_acc(float s, f2 q, f2& acc) {
   f2 ss = f2_make(s, s);
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc.v) : "l"(ss.v), "l"(q.v));
-}
-__device__ __forceinline__ void f2_mul_acc(f2& a, f2 b) {
-  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(a.v) : "l"(b.v));
 }
 
 __device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
@@ -182,18 +159,7 @@ __device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
   return r;
 }
 
-// 16-byte shared load as two packed fp32 pairs
-__device__ __forceinline__ void lds_v4_b64(uint32_t addr, f2& a, f2& b) {
-  asm("ld.shared.v2.b64 {%0, %1}, [%2];" : "=l"(a.v), "=l"(b.v) : "r"(addr));
-}
-__device__ __forceinline__ void lds_b64(uint32_t addr, f2& a) {
-  asm("ld.shared.b64 %0, [%1];" : "=l"(a.v) : "r"(addr));
-}
 
-__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
-  __half2 h = __floats2half2_rn(a, b);
-  return *reinterpret_cast<uint32_t*>(&h);
-}
 
 }  // namespace ptx
 }  // namespace sphkv

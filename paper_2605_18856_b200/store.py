@@ -1,9 +1,10 @@
 """Device-resident paged KV store (drop-in for sphkv.store, pkg/src/sphkv/store.py).
 
 `PagedStore` keeps every page in HBM in the B200 page format described in
-include/sphkv_b200.h: a code pool (coordinate-major angle rows with stride =
-page_size, then the radius row), an fp16 value pool with 16-byte swizzled
-rows, and a page table / pointer lists.  Packing, appending and exporting run
+include/sphkv_b200.h: a code pool (per page the word-interleaved item-major
+angle block -- each item's code string cut into 16-byte quads interleaved
+across 32-item granules -- then the radius row), an fp16 value pool with
+16-byte swizzled rows, and a page table / pointer lists.  Packing, appending and exporting run
 as sm_100a kernels; the host keeps only the reference's accounting model
 (TrafficMeter, ResidentBreakdown -- closed-form byte counts, store.py:51-133)
 and lazily materialized page views for inspection.
