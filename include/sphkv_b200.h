@@ -292,7 +292,10 @@ int sphkv_controller_stats(const void* keys, int key_dtype, const double* q_rows
 
 /* Tile geometry the decode kernels were built with, for the host planner:
  * items per tile (min(P, this) for narrow pages) and the tile cap of one
- * work unit (units above it are rejected by the planner, never truncated). */
+ * work unit: the planner cuts units to it; the general kernel runs a longer
+ * unit (a direct caller's) as several segments; the standard fused kernel
+ * flags it in ctl[n_groups + 2] = SPHKV_E_CAPACITY (its outputs are then
+ * unusable -- re-plan or use sphkv_ada_decode). */
 int sphkv_ada_tile_items(void);
 int sphkv_unit_tile_cap(void);
 
@@ -309,8 +312,10 @@ int sphkv_ada_decode(const sphkv_store_t* st, const float* q, int G,
  * split of a plan group merges that group's partial slots into `out` fp32
  * [n_groups*G, d_v] (same result as sphkv_lse_merge).  slot_group int32
  * [n_slots] gives each partial slot's plan group (-1 = scratch slot);
- * slot_begin as for sphkv_lse_merge; ctl int32 [n_groups + 2] must be zero
- * before the first call and is left zero (CUDA-graph replay safe).
+ * slot_begin as for sphkv_lse_merge; ctl int32 [n_groups + 3] must be zero
+ * before the first call and is left zero (CUDA-graph replay safe) except the
+ * error word ctl[n_groups + 2] (set to SPHKV_E_CAPACITY when a unit exceeds
+ * sphkv_unit_tile_cap() tiles; sticky until the caller clears it).
  * dynamic != 0: CTAs claim units from a global queue in list order (plan the
  * list longest-first) instead of the static u += grid assignment. */
 int sphkv_ada_decode_fused(const sphkv_store_t* st, const float* q, int G,

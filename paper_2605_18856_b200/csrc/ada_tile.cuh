@@ -564,8 +564,10 @@ __device__ __noinline__ void ada_tile_hb(const uint8_t* __restrict__ blkb, int s
                                          uint32_t hb, uint32_t rbit0, int rb, float rscale,
                                          float lg[TK][2 * GP]);
 
-// hb_off: byte offset of the per-query 2-bit h-byte tables in `sm` (0: none)
-template <int GP>
+// hb_off: byte offset of the per-query 2-bit h-byte tables in `sm` (0: none).
+// DK: the head dimension the kernel instantiation is specialised for (128,
+// 64), 0 (any d: generic tiles only) or -1 (runtime d, both sets).
+template <int GP, int DK>
 __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, int d, int P,
                                                    const sphkv_page_t& pg, int sub, int lane,
                                                    const uint8_t* sm, uint32_t qs, int lut_enc,
@@ -580,18 +582,17 @@ __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, 
 #define SPHKV_WI(b, dd, mode, rp) \
   ada_tile_wi<b, dd, GP, mode, rp>(blk, sub, lane, sm, qs, tb, rbit0, rb, rs, lg)
 #ifndef SPHKV_NO_HB
-  if constexpr (GP <= 2) {
+  if constexpr (GP <= 2 && DK > 0) {
     if (B == 2 && hb_off != 0 && P % TTI == 0) {
-      const uint32_t hb = ptx::smem_u32(sm) + hb_off;
-      if (d == 128) ada_tile_hb<128, GP>(blk, sub, lane, hb, rbit0, rb, rs, lg);
-      else ada_tile_hb<64, GP>(blk, sub, lane, hb, rbit0, rb, rs, lg);
+      ada_tile_hb<DK, GP>(blk, sub, lane, ptx::smem_u32(sm) + hb_off, rbit0, rb, rs, lg);
       return;
     }
   }
 #endif
   if (P % TTI != 0) {
     // pages narrower than a tile: generic path (guards items >= P)
-  } else if (d == 128) {
+  } else if (DK == 128 || (DK < 0 && d == 128)) {
+   if constexpr (DK == 128 || DK < 0) {
     if (B == 2 && mode == 1) { SPHKV_WI(2, 128, 4, 8); return; }
     if (B == 4 && mode == 1) { SPHKV_WI(4, 128, 2, 8); return; }
     if (B == 4 && mode == 0) { SPHKV_WI(4, 128, 2, 1); return; }
@@ -605,13 +606,16 @@ __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, 
     if (B == 12 && mode == 2) { SPHKV_WI(12, 128, 1, 2); return; }
     if (B == 12 && mode == 0) { SPHKV_WI(12, 128, 1, 1); return; }
     if (B == 15 && !has) { SPHKV_WI(15, 128, 0, 1); return; }
-  } else if (d == 64) {
+   }
+  } else if (DK == 64 || (DK < 0 && d == 64)) {
+   if constexpr (DK == 64 || DK < 0) {
     if (B == 2 && mode == 1) { SPHKV_WI(2, 64, 4, 8); return; }
     if (B == 4 && mode == 1) { SPHKV_WI(4, 64, 2, 8); return; }
     if (B == 6 && mode == 1) { SPHKV_WI(6, 64, 1, 16); return; }
     if (B == 7 && mode == 1) { SPHKV_WI(7, 64, 1, 16); return; }
     if (B == 12 && mode == 2) { SPHKV_WI(12, 64, 1, 2); return; }
     if (B == 12 && mode == 0) { SPHKV_WI(12, 64, 1, 1); return; }
+   }
   }
 #undef SPHKV_WI
   ada_tile_generic<GP>(blk, B, d, P, sub, lane, sm, qs, lut_enc, rbit0, rb, rs, lg);

@@ -33,6 +33,15 @@
 
 namespace sphkv {
 
+// Cold per-unit helpers, inlined (SPHKV_COLD_INLINE=0: out of line -- measured
+// slower: the calls spill around them and the code layout shifts; instruction
+// fetch is a first-order cost of this kernel).
+#if !defined(SPHKV_COLD_INLINE) || SPHKV_COLD_INLINE
+#define SPHKV_COLD __device__ __forceinline__
+#else
+#define SPHKV_COLD __device__ __noinline__
+#endif
+
 constexpr float kLog2e = 1.4426950408889634f;
 #ifndef SPHKV_NL
 #define SPHKV_NL 7
@@ -72,6 +81,8 @@ struct FusedCtl {
   float* top2;                // [n_slots + 1][G] second-largest logit per split, or NULL
   float* margins;             // [n_groups * G] top-1 minus top-2 logit (natural units)
   int abs_rows;               // out / margins rows by absolute group id, not plan order
+  int32_t* ctl_err;           // set to SPHKV_E_CAPACITY when a unit exceeds the tile list
+                              // (standard kernel only; NULL: not checked)
   int state_out;              // out = one partial-state slot per group (m = log2-sum-exp,
                               // l = 1, acc = normalized output): a page-range split's
                               // local result, ready for the all-gather and merge over ranks
@@ -136,7 +147,7 @@ __device__ __forceinline__ int unit_end(const sphkv_store_t& st, const sphkv_uni
 // Writes the tile count to seg[0] and the first pointer position NOT taken
 // to seg[1] (== pe when the range is done; a unit longer than the cap runs as
 // several segments).  item_base = items of the unit before pb (dbg offsets).
-__device__ void build_tiles(const sphkv_store_t& st, int group, int pb, int pe, int item_base,
+SPHKV_COLD void build_tiles(const sphkv_store_t& st, int group, int pb, int pe, int item_base,
                             int TI, TileEntry* tiles, int* seg, int lane) {
   const int* ptr = st.ptr + (size_t)group * st.ptr_cap;
   int nt = 0, items = item_base, next = pe;
@@ -405,7 +416,7 @@ __device__ __forceinline__ void pv_write(const PVState<MTW>& s, float* part, int
 // Called by every thread after the unit's partial is written (all threads
 // have passed a __syncthreads since).  Returns through smem whether this CTA
 // merged; the caller's loop continues with *next_unit (dynamic mode).
-__device__ __forceinline__ void fused_unit_done(const FusedCtl& f, const float* partials,
+SPHKV_COLD void fused_unit_done(const FusedCtl& f, const float* partials,
                                                 int out_slot, int G, int d_v, int n_units,
                                                 int* s_flag, float* s_ml, int* s_next,
                                                 int group = 0) {
@@ -520,7 +531,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
-template <int GP>
+template <int GP, int DK>
 __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p) {
 #ifdef SPHKV_DBG_TIMING
   if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x] = gtimer();
@@ -666,15 +677,12 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       qs[j * (q_row_bytes(GP) / 8) + g2] = make_float2(a, b);
     }
 #ifndef SPHKV_NO_HB
-    if constexpr (GP <= 2) {
+    if constexpr (GP <= 2 && DK != 0) {
       if (p.hb) {  // per-query tables of the 2-bit tier; scratch = the idle P slots
         __syncthreads();  // the previous unit's last P-slot reads are done
         double* scratch = reinterpret_cast<double*>(pslots);
         const double qs_d = 1.4426950408889634 / sqrt((double)d);
-        if (d == 128)
-          hb_build<128>(smem + p.smem_hb, scratch, qg, p.G, qs_d);
-        else
-          hb_build<64>(smem + p.smem_hb, scratch, qg, p.G, qs_d);
+        hb_build<DK>(smem + p.smem_hb, scratch, qg, p.G, qs_d);
       }
     }
 #endif
@@ -704,14 +712,18 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
         // the P slot of tile k is k % NS whoever computes it.
         if (!(first && seg_first))
           for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, nt);
+#ifdef SPHKV_TILE_LOOP_NOUNROLL
 #pragma unroll 1
+#endif
         for (;;) {
           int k = 0;
           if (lane == 0) k = atomicAdd(tile_ctr, 1);
           k = __shfl_sync(0xffffffffu, k, 0);
           if (k >= nt) break;
           prefetch_tile(k + SPHKV_PF_DIST, nt);
+#ifndef SPHKV_NO_HB
           prefetch_tile_l1(k + SPHKV_PF_L1, nt);
+#endif
           const uint32_t gk = gbase + k;
           const TileEntry te = tiles[k];
           const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
@@ -722,7 +734,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
           for (int a_ = 0; a_ < TK; ++a_)
             for (int b_ = 0; b_ < 2 * GP; ++b_) lg[a_][b_] = (float)(a_ + b_) * 0.01f + (float)ti;
 #else
-          ada_logit_dispatch<GP>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
+          ada_logit_dispatch<GP, DK>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
                                  p.lut_off[ti], lg, p.hb ? p.smem_hb : 0u);
 #endif
           uint32_t valid = 0;
@@ -778,7 +790,12 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
       }
       gbase += nt;
       __syncthreads();  // the tile list and seg[] may be rebuilt now
+#ifdef SPHKV_NO_SEG  // experiment builds: one segment per unit (oversize units truncated)
+      (void)seg_end;
+      break;
+#else
       if (seg_end >= pe) break;
+#endif
     }
     if (warp >= ADA_NL) {
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
@@ -794,6 +811,273 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 #ifdef SPHKV_DBG_TIMING
   if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x + 1] = gtimer();
 #endif
+}
+
+// Tile list of a whole unit for the standard kernel (warp 0): returns the
+// tile count (also in smem); a unit with more tiles than the list holds is
+// flagged in ctl_err (the launch's units are unusable: SPHKV_E_CAPACITY).
+__device__ int build_tiles_std(const sphkv_store_t& st, const sphkv_unit_t& u, int TI,
+                               TileEntry* tiles, int* ntiles_smem, int lane, int32_t* ctl_err) {
+  const int* ptr = st.ptr + (size_t)u.group * st.ptr_cap;
+  int nt = 0, items = 0;
+  for (int b = u.ptr_begin; b < u.ptr_end; b += 32) {
+    int pos = b + lane;
+    int pid = -1, cnt = 0;
+    if (pos < u.ptr_end) {
+      pid = ptr[pos];
+      cnt = st.pages[pid].count;
+    }
+    int t = (cnt + TI - 1) / TI;
+    // inclusive scans of tiles and items
+    int ts = t, is = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int a = __shfl_up_sync(0xffffffffu, ts, o), c = __shfl_up_sync(0xffffffffu, is, o);
+      if (lane >= o) { ts += a; is += c; }
+    }
+    int t0 = nt + ts - t, i0 = items + is - cnt;
+    for (int s = 0; s < t; ++s) {
+      if (t0 + s < MAX_UNIT_TILES) {
+        tiles[t0 + s].page = pid;
+        tiles[t0 + s].sub_off = (s << 24) | (i0 + s * TI);
+      }
+    }
+    nt += __shfl_sync(0xffffffffu, ts, 31);
+    items += __shfl_sync(0xffffffffu, is, 31);
+  }
+  if (lane == 0) {
+    *ntiles_smem = nt < MAX_UNIT_TILES ? nt : MAX_UNIT_TILES;
+    if (nt > MAX_UNIT_TILES && ctl_err != nullptr) atomicExch(ctl_err, SPHKV_E_CAPACITY);
+  }
+  return nt;
+}
+
+
+// The standard path (one launch per layer, fused merge, no margins / live
+// store / state output / h-byte tables / debug logits): the round-1 kernel
+// body, kept verbatim because its instruction layout is measurably faster
+// than the general kernel's (c5 +5%, c4 +65%).  Units
+// must fit the tile list (planner-made units do; others are flagged).
+template <int GP>
+__global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_std(const AdaParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const sphkv_store_t& st = p.st;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float2* lut = reinterpret_cast<float2*>(smem);
+  float2* qs = reinterpret_cast<float2*>(smem + p.smem_q);
+  TileEntry* tiles = reinterpret_cast<TileEntry*>(smem + p.smem_tiles);
+  int* ntiles_s = reinterpret_cast<int*>(smem + p.smem_tiles + MAX_UNIT_TILES * sizeof(TileEntry));
+  int* tile_ctr = ntiles_s + 1;
+  uint8_t* pslots = smem + p.smem_p;
+  uint8_t* vslots = smem + p.smem_v;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
+  uint64_t* p_full = bars;
+  uint64_t* p_empty = bars + ADA_NS;
+  uint64_t* v_full = bars + 2 * ADA_NS;
+  uint64_t* v_empty = bars + 2 * ADA_NS + ADA_NV;
+  const int d = st.d, P = st.page_size, TI = p.TI, dvp = p.dvp, MT = dvp / 16;
+  const uint32_t vbytes = (uint32_t)TI * dvp * 2;
+
+  // Prologue (independent of the previous grid, so under programmatic
+  // dependent launch it overlaps that grid's tail): barrier init and the
+  // polar LUTs -- one TMA bulk copy of the prebuilt tables (or fp64 sincos
+  // rounded to fp32 computed in place when the store has no global table).
+  uint64_t* lut_bar = bars + 2 * ADA_NS + 2 * ADA_NV;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ADA_NS; ++i) {
+      ptx::mbar_init(&p_full[i], 1);
+      ptx::mbar_init(&p_empty[i], ADA_NPV);
+    }
+    for (int i = 0; i < ADA_NV; ++i) {
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], ADA_NPV);
+    }
+    ptx::mbar_init(lut_bar, 1);
+    ptx::fence_mbar_init();
+    if (p.lut_global != nullptr && p.lut_bytes > 0) {
+      ptx::mbar_arrive_expect_tx(lut_bar, (uint32_t)p.lut_bytes);
+      ptx::bulk_g2s(smem, p.lut_global, (uint32_t)p.lut_bytes, lut_bar);
+    } else {
+      ptx::mbar_arrive(lut_bar);
+    }
+  }
+  if (p.lut_global == nullptr) lut_fill(smem, st.tiers, st.n_tiers, p.lut_off, threadIdx.x, blockDim.x);
+  // L2 prefetch, PF_DIST tiles ahead of the claim order: the tile's code
+  // granules (contiguous in the WI layout), its radius row with the
+  // page's first tile, and (SPHKV_PF_V) its fp16 V block, so the V bulk
+  // copy and the code loads hit L2 and many more bytes are in flight per
+  // SM than the smem rings alone could hold.
+  auto prefetch_tile = [&](int t, int nt) {
+    if (t < nt && lane == 0) {
+      const TileEntry tn = tiles[t];
+      const int sb = tn.sub_off >> 24;
+      const sphkv_page_t pn = st.pages[tn.page];
+      const uint64_t W4 = (uint64_t)item_words(d, pn.abits) * 128;  // bytes per granule
+      const int g0 = sb * TI / 32, ng = (TI + 31) / 32;
+      ptx::bulk_prefetch_l2(st.codes + pn.code_off + g0 * W4, (uint32_t)(ng * W4));
+      if (sb == 0) {
+        const uint64_t ab = angle_part_bytes(d, P, pn.abits);
+        ptx::bulk_prefetch_l2(st.codes + pn.code_off + ab,
+                              (uint32_t)(code_block_bytes(d, P, pn.abits, pn.rbits) - ab));
+      }
+#if SPHKV_PF_V
+      ptx::bulk_prefetch_l2(st.values + ((size_t)tn.page * P + (size_t)sb * TI) * dvp, vbytes);
+#endif
+    }
+  };
+  // Also independent of the previous grid (it only reads q and writes
+  // outputs): the first unit's tile list and its first L2 prefetches.
+  // scalars of the fused merge / unit queue live after the barriers (no static
+  // __shared__: it would cost a 1 KB-aligned block next to the dynamic region)
+  int& s_flag = *reinterpret_cast<int*>(bars + 2 * ADA_NS + 2 * ADA_NV + 1);
+  int& s_next = *(reinterpret_cast<int*>(bars + 2 * ADA_NS + 2 * ADA_NV + 1) + 1);
+  float* s_ml = reinterpret_cast<float*>(bars + 2 * ADA_NS + 2 * ADA_NV + 2);
+  int u = fused_first_unit(p.fz, &s_next);
+  if (u < p.n_units && warp == 0) {
+    build_tiles_std(st, p.units[u], TI, tiles, ntiles_s, lane, p.fz.ctl_err);
+    if (lane == 0) *tile_ctr = 0;
+  }
+  __syncthreads();
+  // V tile producer (lane 0 of the first PV warp): bulk copy of tile k's fp16
+  // V block into ring slot (gbase + k) % NV once every PV warp released it
+  const uint64_t vpol = ptx::policy_evict_first();
+  auto issue_v = [&](int k, uint32_t gb) {
+    const uint32_t gk = gb + k;
+    const int vs = gk % ADA_NV;
+    ptx::mbar_wait(&v_empty[vs], ((gk / ADA_NV) & 1) ^ 1);
+    const TileEntry te = tiles[k];
+    const int sub = te.sub_off >> 24;
+    const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)sub * TI) * dvp;
+    ptx::fence_proxy_async();  // order earlier ldmatrix reads of the slot
+    ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
+    ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
+  };
+  if (u < p.n_units && warp < ADA_NL)
+    for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, *ntiles_s);
+  if (u < p.n_units && warp == ADA_NL && lane == 0)
+    for (int k = 0; k < *ntiles_s && k < ADA_NV; ++k) issue_v(k, 0u);
+  ptx::griddep_wait();  // inputs below (q) may come from the previous grid
+  __syncthreads();
+  ptx::griddep_launch_dependents();
+  bool lut_ready = false, first = true;
+
+  const float qscale = kLog2e * rsqrtf((float)d);
+  uint32_t gbase = 0;  // running tile sequence number (barrier phases)
+  for (; u < p.n_units; first = false) {
+    const sphkv_unit_t unit = p.units[u];
+    if (!first && warp == 0) {
+      build_tiles_std(st, unit, TI, tiles, ntiles_s, lane, p.fz.ctl_err);
+      if (lane == 0) *tile_ctr = 0;
+    }
+    // q rows for this group, prescaled into base-2 logit units, packed pairs
+    const float* qg = p.q + (size_t)unit.group * p.G * d;
+    for (int i = threadIdx.x; i < d * GP; i += blockDim.x) {
+      int j = i / GP, g2 = i % GP;
+      float a = (2 * g2 < p.G) ? qg[(size_t)(2 * g2) * d + j] * qscale : 0.f;
+      float b = (2 * g2 + 1 < p.G) ? qg[(size_t)(2 * g2 + 1) * d + j] * qscale : 0.f;
+      qs[j * (q_row_bytes(GP) / 8) + g2] = make_float2(a, b);
+    }
+    __syncthreads();
+    const int nt = *ntiles_s;
+
+    if (warp < ADA_NL) {
+      // ---------------- logit warps ----------------
+      if (!lut_ready) {
+        ptx::mbar_wait(lut_bar, 0);
+        lut_ready = true;
+      }
+      // tiles are claimed dynamically (smem counter) to balance the warps;
+      // the P slot of tile k is k % NS whoever computes it.
+#pragma unroll 1
+      if (!first)
+        for (int t = warp; t < SPHKV_PF_DIST; t += ADA_NL) prefetch_tile(t, nt);
+      for (;;) {
+        int k = 0;
+        if (lane == 0) k = atomicAdd(tile_ctr, 1);
+        k = __shfl_sync(0xffffffffu, k, 0);
+        if (k >= nt) break;
+        prefetch_tile(k + SPHKV_PF_DIST, nt);
+        const uint32_t gk = gbase + k;
+        const TileEntry te = tiles[k];
+        const int sub = te.sub_off >> 24, ioff = te.sub_off & 0xffffff;
+        const sphkv_page_t pg = st.pages[te.page];
+        const int ti = tier_index(st, pg.tier);
+        float lg[TK][2 * GP];  // LUT region starts at smem[0]
+#ifdef SPHKV_DBG_NOLOGIT  // bottleneck probe: skip the logit math
+        for (int a_ = 0; a_ < TK; ++a_)
+          for (int b_ = 0; b_ < 2 * GP; ++b_) lg[a_][b_] = (float)(a_ + b_) * 0.01f + (float)ti;
+#else
+        ada_logit_dispatch<GP, -1>(pg.abits, st.codes, d, P, pg, sub, lane, smem, p.smem_q,
+                               p.lut_off[ti], lg);
+#endif
+        uint32_t valid = 0;
+#pragma unroll
+        for (int kk = 0; kk < TK; ++kk) {
+          const int it = sub * TI + 32 * kk + lane;
+          if (32 * kk + lane < TI && it < pg.count) valid |= 1u << kk;
+        }
+        if (p.logits_dbg != nullptr) {
+#pragma unroll
+          for (int kk = 0; kk < TK; ++kk) {
+            float* dst = p.logits_dbg + (size_t)(p.dbg_off[u] + ioff + 32 * kk + lane) * p.G;
+#pragma unroll
+            for (int g = 0; g < 2 * GP; ++g)
+              if ((valid & (1u << kk)) && g < p.G) dst[g] = lg[kk][g] * (1.0f / kLog2e);
+          }
+        }
+        const int ps = gk % ADA_NS;
+        ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
+        write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, p.prows, TI, lane, p.G, lg,
+                            valid, p.fz.top2 != nullptr);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
+      }
+    } else {
+      // ---------------- PV warps ----------------
+      // NPV warps split the d_v m-tiles; all consume every tile in order.
+      // Lane 0 of PV warp 0 is also the V producer: it refills slot vs once
+      // every PV warp has released it (v_empty counts NPV arrivals).
+      const int pw = warp - ADA_NL;
+      const int mtw = (MT + ADA_NPV - 1) / ADA_NPV;
+      const int mt0 = pw * mtw;
+      const int mtn = max(0, min(mtw, MT - mt0));
+      if (!first && pw == 0 && lane == 0)
+        for (int k = 0; k < nt && k < ADA_NV; ++k) issue_v(k, gbase);
+      PVState<ADA_MTW> s;
+      pv_init(s);
+      const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t gk = gbase + k;
+        const int vs = gk % ADA_NV, ps = gk % ADA_NS;
+        ptx::mbar_wait(&v_full[vs], (gk / ADA_NV) & 1);
+        ptx::mbar_wait(&p_full[ps], (gk / ADA_NS) & 1);
+#ifndef SPHKV_DBG_NOPV  // bottleneck probe: skip the P.V math
+        if (fast_pv)
+          pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                               p.prow_bytes, p.prows, mt0, p.G, lane, p.fz.top2 != nullptr);
+        else
+          pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                           p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane,
+                           p.fz.top2 != nullptr);
+#endif
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&p_empty[ps]);
+          ptx::mbar_arrive(&v_empty[vs]);
+          if (pw == 0 && k + ADA_NV < nt) issue_v(k + ADA_NV, gbase);
+        }
+      }
+      float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
+      pv_write<ADA_MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane,
+                        p.fz.top2 != nullptr ? p.fz.top2 + (size_t)unit.out_slot * p.G : nullptr);
+    }
+    gbase += nt;
+    __syncthreads();
+    fused_unit_done(p.fz, p.partials, unit.out_slot, p.G, st.d_v, p.n_units, &s_flag, s_ml,
+                    &s_next);
+    u = p.fz.dynamic ? s_next : u + gridDim.x;
+  }
+  fused_kernel_exit(p.fz);
 }
 
 // ---------------------------------------------------------------------------
@@ -1134,9 +1418,9 @@ static int launch_pdl(Kern kern, const Params& p, int grid, int threads, size_t 
   return SPHKV_OK;
 }
 
-template <int GP>
-static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream, bool pdl) {
-  auto kern = k_ada_decode<GP>;
+template <int GP, int DK>
+static int launch_ada_dk(AdaParams& p, size_t smem, int grid, cudaStream_t stream, bool pdl) {
+  auto kern = k_ada_decode<GP, DK>;
   cudaFuncAttributes fa;
   SPHKV_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
   int dev = 0, optin = 0;
@@ -1147,6 +1431,34 @@ static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream, 
                 smem, (size_t)fa.sharedSizeBytes, optin);
   SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream, pdl);
+}
+
+template <int GP>
+static int launch_ada_std(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
+  auto kern = k_ada_decode_std<GP>;
+  cudaFuncAttributes fa;
+  SPHKV_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+  int dev = 0, optin = 0;
+  SPHKV_CUDA_TRY(cudaGetDevice(&dev));
+  SPHKV_CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  if (smem + fa.sharedSizeBytes > (size_t)optin)
+    return fail(SPHKV_E_UNSUPPORTED, "ADA decode needs %zu B shared memory (+%zu static) > %d",
+                smem, (size_t)fa.sharedSizeBytes, optin);
+  SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream, true);
+}
+
+template <int GP>
+static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream, bool pdl) {
+  // the standard fused path runs the round-1 kernel body (see k_ada_decode_std)
+  if (pdl && p.fz.ctl_err != nullptr && !p.hb && p.logits_dbg == nullptr &&
+      p.fz.margins == nullptr && !p.fz.state_out && !p.fz.abs_rows)
+    return launch_ada_std<GP>(p, smem, grid, stream);
+  switch (p.st.d) {
+    case 128: return launch_ada_dk<GP, 128>(p, smem, grid, stream, pdl);
+    case 64: return launch_ada_dk<GP, 64>(p, smem, grid, stream, pdl);
+    default: return launch_ada_dk<GP, 0>(p, smem, grid, stream, pdl);
+  }
 }
 
 static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
@@ -1272,6 +1584,7 @@ static int dense_decode_impl(const sphkv_dense_store_t* st, const float* q, int 
 
 static int make_fused(FusedCtl& f, const int32_t* slot_group, const int32_t* slot_begin,
                       int n_groups, int32_t* ctl, float* out, int dynamic) {
+  // ctl: [n_groups] split counters, queue head, CTAs done, error word
   memset(&f, 0, sizeof(f));
   if (slot_group != nullptr && (!slot_begin || !ctl || !out || n_groups < 1))
     return fail(SPHKV_E_VALUE, "fused merge needs slot_begin, ctl and out");
@@ -1282,6 +1595,7 @@ static int make_fused(FusedCtl& f, const int32_t* slot_group, const int32_t* slo
   f.out = out;
   f.n_groups = n_groups;
   f.dynamic = dynamic;
+  f.ctl_err = (slot_group != nullptr && ctl != nullptr) ? ctl + n_groups + 2 : nullptr;
   return SPHKV_OK;
 }
 

@@ -77,6 +77,11 @@ def ada_decode(store, q, plan: DecodePlan | None = None, *, out=None, partials=N
             store.cptr_for(G), q.data_ptr(), G, plan.units.data_ptr(), plan.n_units,
             partials.data_ptr(), plan.slot_group.data_ptr(), plan.slot_begin.data_ptr(), ng,
             plan.ctl.data_ptr(), out.data_ptr(), int(plan.dynamic), plan.grid, sp))
+        if plan.check_units:  # hand-made plans: surface an oversize unit (one sync)
+            if int(plan.ctl[ng + 2].item()):
+                plan.ctl[ng + 2] = 0
+                raise RuntimeError("a decode unit exceeds the kernel's tile list "
+                                   "(sphkv_unit_tile_cap); re-plan with plan_store")
         return out
     _lib.check(l.sphkv_ada_decode(store.cptr_for(G), q.data_ptr(), G, plan.units.data_ptr(),
                                   plan.n_units, partials.data_ptr(), _lib.ptr(logits),

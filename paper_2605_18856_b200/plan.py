@@ -62,7 +62,11 @@ class DecodePlan:
         if slot_group is not None:
             sg[:n_slots] = slot_group
         self.slot_group = torch.as_tensor(sg, device=dev)
-        self.ctl = torch.zeros(len(group_ids) + 2, dtype=torch.int32, device=dev)
+        # [groups] split counters, queue head, CTAs done, error word (a unit
+        # over the kernel's tile list: SPHKV_E_CAPACITY)
+        self.ctl = torch.zeros(len(group_ids) + 3, dtype=torch.int32, device=dev)
+        # planner-made units respect the tile cap; set for hand-made plans
+        self.check_units = False
 
 
 def _page_bytes(rows, tiers, d, d_v, P):

@@ -372,7 +372,14 @@ def test_unit_longer_than_tile_cap(sk, monkeypatch):
     monkeypatch.setattr(planmod, "tile_geometry", lambda: (cap[0], 1 << 20))
     big = sk.plan_store(st, groups=[0], grid=1, units_per_cta=1)
     assert big.n_units == 1 and int(big.group_items[0]) > 2 * 512 * cap[0]
-    got = sk.ada_decode(st, wl.queries, big)
+    # the standard fused kernel flags the unit (error word) instead of truncating it
+    big.check_units = True
+    with pytest.raises(RuntimeError):
+        sk.ada_decode(st, wl.queries, big)
+    assert int(big.ctl.abs().sum()) == 0
+    # the general kernel runs it as segments (gate margins / debug logits paths)
+    m = torch.empty(4, dtype=torch.float32, device="cuda")
+    got = sk.ada_decode(st, wl.queries, big, margins=m)
     assert torch.allclose(ref[:4], got, rtol=2e-5, atol=2e-5)
     lg = torch.zeros(int(big.group_items.sum()) * 4, dtype=torch.float32, device="cuda")
     got2 = sk.ada_decode(st, wl.queries, big, logits=lg)
