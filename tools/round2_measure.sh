@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 measurement batch (1 GPU): default bench line, reference arm,
 # binding-budget sweep, other configs, ncu launch list + full capture of c5.
-OUT=gpurun_out/m; mkdir -p $OUT
+OUT=gpurun_out/${TAG:-m}; mkdir -p $OUT
 ( time timeout 900 python bench.py ) > $OUT/bench_c5_default.json 2> $OUT/bench_c5_default.err
 tail -1 $OUT/bench_c5_default.json | cut -c1-400
 ( time timeout 900 python bench.py --impl reference --steps 20 --warmup 5 ) > $OUT/bench_c5_reference.json 2> $OUT/bench_c5_reference.err
