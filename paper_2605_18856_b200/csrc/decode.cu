@@ -327,10 +327,10 @@ __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, c
 }
 
 // Fast path of pv_tile for d_v = 128 (16 swizzled chunks per V row), a
-// 128-item tile and all of the warp's m-tiles present: fully unrolled, every
+// 16*KS-item tile and all of the warp's m-tiles present: fully unrolled, every
 // ldmatrix address is a per-lane base + an immediate (the XOR swizzle term
 // only depends on the row inside the 8-row group, not on the k-step).
-template <int MTW>
+template <int MTW, int KS = ADA_TI / 16>
 __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslot,
                                             const uint8_t* vslot, int prow_bytes, int prows,
                                             int mt0, int G, int lane, bool want2 = false) {
@@ -349,7 +349,7 @@ __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslo
     va[i] = ptx::smem_u32(vslot) + ((r + (mat >> 1) * 8) * 128 + (chunk ^ r) * 8) * 2;
   }
 #pragma unroll
-  for (int ks = 0; ks < ADA_TI / 16; ++ks) {
+  for (int ks = 0; ks < KS; ++ks) {
     uint32_t b0, b1;
     ptx::ldsm_x2(pb + ks * 32, b0, b1);
 #pragma unroll
@@ -1085,10 +1085,23 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_std(const AdaPara
 // ---------------------------------------------------------------------------
 constexpr int DN_NL = 4;
 constexpr int DN_TI = 64;
-constexpr int DN_NK = 8;
-constexpr int DN_NV = 4;
+#ifndef SPHKV_DN_NK
+#define SPHKV_DN_NK 8
+#endif
+#ifndef SPHKV_DN_NV
+#define SPHKV_DN_NV 4
+#endif
+constexpr int DN_NK = SPHKV_DN_NK;  // K ring slots (64-item tiles)
+constexpr int DN_NV = SPHKV_DN_NV;  // V ring slots
 constexpr int DN_NS = 8;
-constexpr int DN_THREADS = (DN_NL + 2) * 32;
+// Two launch shapes (dense_threads): d_v = 128 runs two PV warps (each half
+// of the d_v m-tiles) and separate K and V producer warps -- a single
+// producer blocked on a full V ring starved the logit warps of K (c5:
+// 0.77 -> 0.84 of the copy peak); narrower values keep one PV warp and one
+// producer, which measured faster there (c4, d_v = 64).
+__host__ __device__ constexpr int dense_threads(int npv, bool sep) {
+  return (DN_NL + npv + (sep ? 2 : 1)) * 32;
+}
 
 struct DenseParams {
   sphkv_dense_store_t st;
@@ -1104,7 +1117,9 @@ struct DenseParams {
   FusedCtl fz;
 };
 
-__global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParams p) {
+template <int NPV, bool SEP>  // SEP also selects the unrolled d_v = 128 P.V
+__global__ void __launch_bounds__(dense_threads(NPV, SEP), 1) k_dense_decode(const DenseParams p) {
+  constexpr int MTW = 8 / NPV;
   extern __shared__ __align__(128) uint8_t smem[];
   const sphkv_dense_store_t& st = p.st;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1124,8 +1139,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < DN_NK; ++i) { ptx::mbar_init(&k_full[i], 1); ptx::mbar_init(&k_empty[i], 1); }
-    for (int i = 0; i < DN_NV; ++i) { ptx::mbar_init(&v_full[i], 1); ptx::mbar_init(&v_empty[i], 1); }
-    for (int i = 0; i < DN_NS; ++i) { ptx::mbar_init(&p_full[i], 1); ptx::mbar_init(&p_empty[i], 1); }
+    for (int i = 0; i < DN_NV; ++i) { ptx::mbar_init(&v_full[i], 1); ptx::mbar_init(&v_empty[i], NPV); }
+    for (int i = 0; i < DN_NS; ++i) { ptx::mbar_init(&p_full[i], 1); ptx::mbar_init(&p_empty[i], NPV); }
     ptx::fence_mbar_init();
   }
   ptx::griddep_wait();  // same PDL contract as the ADA kernel
@@ -1229,16 +1244,25 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
       }
-    } else if (warp == DN_NL) {
-      PVState<8> s;
+    } else if (warp < DN_NL + NPV) {
+      // NPV warps split the d_v m-tiles; each consumes every tile
+      const int pw = warp - DN_NL;
+      const int mt0 = NPV == 1 ? 0 : pw * MTW;  // compile-time 0 with one PV warp
+      const int mtn = max(0, min(MTW, MT - mt0));
+      PVState<MTW> s;
       pv_init(s);
       for (int k = 0; k < nt; ++k) {
         const uint32_t gk = gbase + k;
         const int vs = gk % DN_NV, ps = gk % DN_NS;
         ptx::mbar_wait(&v_full[vs], (gk / DN_NV) & 1);
         ptx::mbar_wait(&p_full[ps], (gk / DN_NS) & 1);
-        pv_tile<8>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes, p.prow_bytes, 8,
-                   DN_TI, dvp, 0, MT, p.G, lane);
+        if constexpr (SEP)  // launched for d_v = 128 only
+          pv_tile_128<MTW, DN_TI / 16>(s, pslots + ps * p.pslot_bytes,
+                                          vslots + (size_t)vs * vbytes, p.prow_bytes, 8, mt0,
+                                          p.G, lane);
+        else
+          pv_tile<MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                          p.prow_bytes, 8, DN_TI, dvp, mt0, mtn, p.G, lane);
         __syncwarp();
         if (lane == 0) {
           ptx::mbar_arrive(&p_empty[ps]);
@@ -1246,16 +1270,35 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_decode(const DenseParam
         }
       }
       float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
-      pv_write<8>(s, part, p.G, st.d_v, 0, MT, true, lane);
-    } else if (lane == 0) {
+      pv_write<MTW>(s, part, p.G, st.d_v, mt0, mtn, pw == 0, lane);
+    } else if (!SEP) {
+      if (lane == 0) {
+        for (int k = 0; k < nt; ++k) {
+          const uint32_t gk = gbase + k;
+          const int ks = gk % DN_NK, vs = gk % DN_NV;
+          const size_t item0 = gpage0 * P + (size_t)(t_begin + k) * DN_TI;
+          ptx::mbar_wait(&k_empty[ks], ((gk / DN_NK) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&k_full[ks], kbytes);
+          ptx::bulk_g2s(kslots + (size_t)ks * kbytes, st.keys + item0 * dp, kbytes, &k_full[ks]);
+          ptx::mbar_wait(&v_empty[vs], ((gk / DN_NV) & 1) ^ 1);
+          ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
+          ptx::bulk_g2s(vslots + (size_t)vs * vbytes, st.values + item0 * dvp, vbytes, &v_full[vs]);
+        }
+      }
+    } else if (lane == 0 && warp == DN_NL + NPV) {  // K producer
       for (int k = 0; k < nt; ++k) {
         const uint32_t gk = gbase + k;
-        const int ks = gk % DN_NK, vs = gk % DN_NV;
-        const size_t tile = (size_t)(t_begin + k);
-        const size_t item0 = gpage0 * P + tile * DN_TI;
+        const int ks = gk % DN_NK;
+        const size_t item0 = gpage0 * P + (size_t)(t_begin + k) * DN_TI;
         ptx::mbar_wait(&k_empty[ks], ((gk / DN_NK) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&k_full[ks], kbytes);
         ptx::bulk_g2s(kslots + (size_t)ks * kbytes, st.keys + item0 * dp, kbytes, &k_full[ks]);
+      }
+    } else if (lane == 0) {  // V producer
+      for (int k = 0; k < nt; ++k) {
+        const uint32_t gk = gbase + k;
+        const int vs = gk % DN_NV;
+        const size_t item0 = gpage0 * P + (size_t)(t_begin + k) * DN_TI;
         ptx::mbar_wait(&v_empty[vs], ((gk / DN_NV) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
         ptx::bulk_g2s(vslots + (size_t)vs * vbytes, st.values + item0 * dvp, vbytes, &v_full[vs]);
@@ -1575,11 +1618,16 @@ static int dense_decode_impl(const sphkv_dense_store_t* st, const float* q, int 
   off += (2 * DN_NK + 2 * DN_NV + 2 * DN_NS) * 8;
   size_t smem = off;
   if (smem > 227 * 1024) return fail(SPHKV_E_UNSUPPORTED, "dense smem %zu exceeds 227 KB", smem);
-  SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
   if (grid <= 0) grid = SM_COUNT;
   if (grid > n_units) grid = n_units;
-  return launch_pdl(k_dense_decode, p, grid, DN_THREADS, smem, stream);
+  if (p.dvp == 128) {
+    SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode<2, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return launch_pdl(k_dense_decode<2, true>, p, grid, dense_threads(2, true), smem, stream);
+  }
+  SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode<1, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return launch_pdl(k_dense_decode<1, false>, p, grid, dense_threads(1, false), smem, stream);
 }
 
 static int make_fused(FusedCtl& f, const int32_t* slot_group, const int32_t* slot_begin,
