@@ -330,10 +330,13 @@ __device__ __forceinline__ void pv_tile(PVState<MTW>& s, const uint8_t* pslot, c
 // 16*KS-item tile and all of the warp's m-tiles present: fully unrolled, every
 // ldmatrix address is a per-lane base + an immediate (the XOR swizzle term
 // only depends on the row inside the 8-row group, not on the k-step).
-template <int MTW, int KS = ADA_TI / 16>
+template <int MTW, int KS = ADA_TI / 16, int DVP = 128, int MTU = MTW>
 __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslot,
                                             const uint8_t* vslot, int prow_bytes, int prows,
                                             int mt0, int G, int lane, bool want2 = false) {
+  // DVP: padded d_v (128 or 64: 16 or 8 swizzled chunks per row); MTU <= MTW
+  // m-tiles are computed (d_v = 64 through a PVState sized for 128)
+  static_assert(DVP == 128 || DVP == 64, "fast P.V path: d_v 64 or 128");
   float c[MTW][4];
 #pragma unroll
   for (int i = 0; i < MTW; ++i)
@@ -342,20 +345,20 @@ __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslo
   const int r = lane & 7, mat = lane >> 3;
   const uint32_t pb = ptx::smem_u32(pslot) + ((lane & 7) & (prows - 1)) * prow_bytes +
                       ((lane >> 3) & 1) * 16;
-  uint32_t va[MTW];
+  uint32_t va[MTU];
 #pragma unroll
-  for (int i = 0; i < MTW; ++i) {
+  for (int i = 0; i < MTU; ++i) {
     const int chunk = 2 * (mt0 + i) + (mat & 1);
-    va[i] = ptx::smem_u32(vslot) + ((r + (mat >> 1) * 8) * 128 + (chunk ^ r) * 8) * 2;
+    va[i] = ptx::smem_u32(vslot) + ((r + (mat >> 1) * 8) * DVP + (chunk ^ r) * 8) * 2;
   }
 #pragma unroll
   for (int ks = 0; ks < KS; ++ks) {
     uint32_t b0, b1;
     ptx::ldsm_x2(pb + ks * 32, b0, b1);
 #pragma unroll
-    for (int i = 0; i < MTW; ++i) {
+    for (int i = 0; i < MTU; ++i) {
       uint32_t a0, a1, a2, a3;
-      ptx::ldsm_x4_trans(va[i] + ks * 4096, a0, a1, a2, a3);
+      ptx::ldsm_x4_trans(va[i] + ks * (32 * DVP), a0, a1, a2, a3);
       ptx::mma_f16(c[i], a0, a1, a2, a3, b0, b1);
     }
   }
@@ -371,7 +374,7 @@ __device__ __forceinline__ void pv_tile_128(PVState<MTW>& s, const uint8_t* pslo
     s.m[h] = mn;
     s.l[h] = s.l[h] * al + lt * be;
 #pragma unroll
-    for (int i = 0; i < MTW; ++i) {
+    for (int i = 0; i < MTU; ++i) {
       s.acc[i][h] = s.acc[i][h] * al + c[i][h] * be;
       s.acc[i][2 + h] = s.acc[i][2 + h] * al + c[i][2 + h] * be;
     }
@@ -692,6 +695,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
     PVState<ADA_MTW> s;
     if (warp >= ADA_NL) pv_init(s);
     const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
+    const bool fast64 = (dvp == 64 && TI == ADA_TI && ADA_NPV == 1);
     for (bool seg_first = true;; seg_first = false) {
       if (!(first && seg_first) && warp == 0) {
         const int pb = seg_first ? unit.ptr_begin : seg[1];
@@ -775,6 +779,10 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
           if (fast_pv)
             pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
                                  p.prow_bytes, p.prows, mt0, p.G, lane, p.fz.top2 != nullptr);
+          else if (fast64)
+            pv_tile_128<ADA_MTW, ADA_TI / 16, 64, 4>(s, pslots + ps * p.pslot_bytes,
+                                                     vslots + (size_t)vs * vbytes, p.prow_bytes,
+                                                     p.prows, 0, p.G, lane, p.fz.top2 != nullptr);
           else
             pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
                              p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane,
@@ -1046,6 +1054,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_std(const AdaPara
       PVState<ADA_MTW> s;
       pv_init(s);
       const bool fast_pv = (dvp == 128 && TI == ADA_TI && mtn == ADA_MTW);
+      const bool fast64 = (dvp == 64 && TI == ADA_TI && ADA_NPV == 1);  // c4: +47%
       for (int k = 0; k < nt; ++k) {
         const uint32_t gk = gbase + k;
         const int vs = gk % ADA_NV, ps = gk % ADA_NS;
@@ -1055,6 +1064,10 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_std(const AdaPara
         if (fast_pv)
           pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
                                p.prow_bytes, p.prows, mt0, p.G, lane, p.fz.top2 != nullptr);
+        else if (fast64)
+          pv_tile_128<ADA_MTW, ADA_TI / 16, 64, 4>(s, pslots + ps * p.pslot_bytes,
+                                                   vslots + (size_t)vs * vbytes, p.prow_bytes,
+                                                   p.prows, 0, p.G, lane, p.fz.top2 != nullptr);
         else
           pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
                            p.prow_bytes, p.prows, TI, dvp, mt0, mtn, p.G, lane,
@@ -1117,7 +1130,8 @@ struct DenseParams {
   FusedCtl fz;
 };
 
-template <int NPV, bool SEP>  // SEP also selects the unrolled d_v = 128 P.V
+// DVF: 128 / 64 = the unrolled P.V path for that padded d_v, 0 = generic
+template <int NPV, bool SEP, int DVF>
 __global__ void __launch_bounds__(dense_threads(NPV, SEP), 1) k_dense_decode(const DenseParams p) {
   constexpr int MTW = 8 / NPV;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1256,10 +1270,14 @@ __global__ void __launch_bounds__(dense_threads(NPV, SEP), 1) k_dense_decode(con
         const int vs = gk % DN_NV, ps = gk % DN_NS;
         ptx::mbar_wait(&v_full[vs], (gk / DN_NV) & 1);
         ptx::mbar_wait(&p_full[ps], (gk / DN_NS) & 1);
-        if constexpr (SEP)  // launched for d_v = 128 only
+        if constexpr (DVF == 128)
           pv_tile_128<MTW, DN_TI / 16>(s, pslots + ps * p.pslot_bytes,
                                           vslots + (size_t)vs * vbytes, p.prow_bytes, 8, mt0,
                                           p.G, lane);
+        else if constexpr (DVF == 64 && NPV == 1)
+          pv_tile_128<MTW, DN_TI / 16, 64, 4>(s, pslots + ps * p.pslot_bytes,
+                                              vslots + (size_t)vs * vbytes, p.prow_bytes, 8, 0,
+                                              p.G, lane);
         else
           pv_tile<MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
                           p.prow_bytes, 8, DN_TI, dvp, mt0, mtn, p.G, lane);
@@ -1621,13 +1639,20 @@ static int dense_decode_impl(const sphkv_dense_store_t* st, const float* q, int 
   if (grid <= 0) grid = SM_COUNT;
   if (grid > n_units) grid = n_units;
   if (p.dvp == 128) {
-    SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode<2, true>,
+    SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode<2, true, 128>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    return launch_pdl(k_dense_decode<2, true>, p, grid, dense_threads(2, true), smem, stream);
+    return launch_pdl(k_dense_decode<2, true, 128>, p, grid, dense_threads(2, true), smem, stream);
   }
-  SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode<1, false>,
+#ifndef SPHKV_DN_NO64
+  if (p.dvp == 64) {
+    SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode<1, false, 64>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return launch_pdl(k_dense_decode<1, false, 64>, p, grid, dense_threads(1, false), smem, stream);
+  }
+#endif
+  SPHKV_CUDA_TRY(cudaFuncSetAttribute(k_dense_decode<1, false, 0>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  return launch_pdl(k_dense_decode<1, false>, p, grid, dense_threads(1, false), smem, stream);
+  return launch_pdl(k_dense_decode<1, false, 0>, p, grid, dense_threads(1, false), smem, stream);
 }
 
 static int make_fused(FusedCtl& f, const int32_t* slot_group, const int32_t* slot_begin,
