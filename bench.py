@@ -440,6 +440,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--profile", action="store_true", help="few steps, no graphs (for ncu)")
+    ap.add_argument("--open-reserve", type=float, default=16.0,
+                    help="decode steps with appends: tiles of prefill the last unit of each "
+                    "group leaves for the appended pages (plan_store open_reserve_tiles)")
     ap.add_argument("--no-appends", action="store_true",
                     help="skip the full decode steps (attention + gate + append scoring + "
                          "append of one new key per group, rollout.DecodeStepper)")
@@ -765,7 +768,8 @@ def main():
             torch.randn((groups, d), generator=gen, device="cuda"), dim=-1)) * 1.0
         vn = torch.randn((nsteps + 3, groups, d), generator=gen, device="cuda").half()
         stp = sk.DecodeStepper(st, G, W["u_hat"], W["s_hat"], W["r_q"], lam=synthm.PANEL_LAMBDA,
-                               omega=synthm.PANEL_OMEGA[2], gate_cfg=GateConfig(0.05, 0.5))
+                               omega=synthm.PANEL_OMEGA[2], gate_cfg=GateConfig(0.05, 0.5),
+                               open_reserve_tiles=args.open_reserve)
         stp.capture(stream)
         for t in range(3):
             stp.step(q, kn[t], vn[t], T + t)

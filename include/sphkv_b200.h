@@ -384,7 +384,11 @@ int sphkv_decode_gate(const sphkv_store_t* st, const void* keys, int key_dtype, 
  * previous work on the stream may have changed the store (an append): no
  * programmatic-dependent launch, the prologue may not read the page table
  * early; SPHKV_LIVE_ABS_ROWS -- out [groups*G, d_v] and margins [groups*G]
- * rows are indexed by absolute group id (one buffer for all layer launches). */
+ * rows are indexed by absolute group id (one buffer for all layer launches).
+ * As with sphkv_ada_decode_fused, a unit whose pages exceed
+ * sphkv_unit_tile_cap() tiles is not decoded: ctl[n_groups + 2] is set to
+ * SPHKV_E_CAPACITY (the caller re-plans; planner units of a growing store stay
+ * far below the cap). */
 enum { SPHKV_LIVE_AFTER_MUTATION = 1, SPHKV_LIVE_ABS_ROWS = 2 };
 int sphkv_ada_decode_live(const sphkv_store_t* st, const float* q, int G,
                           const sphkv_unit_t* units, int n_units, float* partials,

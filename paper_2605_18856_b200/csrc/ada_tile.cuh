@@ -605,7 +605,10 @@ __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, 
 #endif
     if (B == 12 && mode == 2) { SPHKV_WI(12, 128, 1, 2); return; }
     if (B == 12 && mode == 0) { SPHKV_WI(12, 128, 1, 1); return; }
-    if (B == 15 && !has) { SPHKV_WI(15, 128, 0, 1); return; }
+    // 13..16 bits have no table: MUFU sin/cos of the fp32 angle (abs error
+    // ~5e-7 per row) -- the reference's max tier, which protected heads append
+    // at during decode; sincospif cost ~4x as much per row
+    if (B == 15 && !has) { SPHKV_WI(15, 128, 3, 1); return; }
    }
   } else if (DK == 64 || (DK < 0 && d == 64)) {
    if constexpr (DK == 64 || DK < 0) {
@@ -615,6 +618,7 @@ __device__ __forceinline__ void ada_logit_dispatch(int B, const uint8_t* codes, 
     if (B == 7 && mode == 1) { SPHKV_WI(7, 64, 1, 16); return; }
     if (B == 12 && mode == 2) { SPHKV_WI(12, 64, 1, 2); return; }
     if (B == 12 && mode == 0) { SPHKV_WI(12, 64, 1, 1); return; }
+    if (B == 15 && !has) { SPHKV_WI(15, 64, 3, 1); return; }
    }
   }
 #undef SPHKV_WI

@@ -86,6 +86,8 @@ struct FusedCtl {
   int state_out;              // out = one partial-state slot per group (m = log2-sum-exp,
                               // l = 1, acc = normalized output): a page-range split's
                               // local result, ready for the all-gather and merge over ranks
+  int flag_units;             // entry point contract: a unit over the tile list is flagged
+                              // in ctl_err (standard kernel) instead of run as segments
 };
 
 struct AdaParams {
@@ -827,11 +829,12 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 __device__ int build_tiles_std(const sphkv_store_t& st, const sphkv_unit_t& u, int TI,
                                TileEntry* tiles, int* ntiles_smem, int lane, int32_t* ctl_err) {
   const int* ptr = st.ptr + (size_t)u.group * st.ptr_cap;
+  const int pe = unit_end(st, u);  // open-ended (live) units: the list's current end
   int nt = 0, items = 0;
-  for (int b = u.ptr_begin; b < u.ptr_end; b += 32) {
+  for (int b = u.ptr_begin; b < pe; b += 32) {
     int pos = b + lane;
     int pid = -1, cnt = 0;
-    if (pos < u.ptr_end) {
+    if (pos < pe) {
       pid = ptr[pos];
       cnt = st.pages[pid].count;
     }
@@ -1087,7 +1090,7 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_std(const AdaPara
     gbase += nt;
     __syncthreads();
     fused_unit_done(p.fz, p.partials, unit.out_slot, p.G, st.d_v, p.n_units, &s_flag, s_ml,
-                    &s_next);
+                    &s_next, unit.group);
     u = p.fz.dynamic ? s_next : u + gridDim.x;
   }
   fused_kernel_exit(p.fz);
@@ -1495,7 +1498,7 @@ static int launch_ada_dk(AdaParams& p, size_t smem, int grid, cudaStream_t strea
 }
 
 template <int GP>
-static int launch_ada_std(AdaParams& p, size_t smem, int grid, cudaStream_t stream) {
+static int launch_ada_std(AdaParams& p, size_t smem, int grid, cudaStream_t stream, bool pdl) {
   auto kern = k_ada_decode_std<GP>;
   cudaFuncAttributes fa;
   SPHKV_CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
@@ -1506,15 +1509,17 @@ static int launch_ada_std(AdaParams& p, size_t smem, int grid, cudaStream_t stre
     return fail(SPHKV_E_UNSUPPORTED, "ADA decode needs %zu B shared memory (+%zu static) > %d",
                 smem, (size_t)fa.sharedSizeBytes, optin);
   SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream, true);
+  return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream, pdl);
 }
 
 template <int GP>
 static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream, bool pdl) {
-  // the standard fused path runs the round-1 kernel body (see k_ada_decode_std)
-  if (pdl && p.fz.ctl_err != nullptr && !p.hb && p.logits_dbg == nullptr &&
-      p.fz.margins == nullptr && !p.fz.state_out && !p.fz.abs_rows)
-    return launch_ada_std<GP>(p, smem, grid, stream);
+  // the fused path (outputs, gate margins, absolute rows, live units) runs the
+  // round-1 kernel body (see k_ada_decode_std); state output, debug logits
+  // and the h-byte tables take the general kernel
+  if (p.fz.flag_units && p.fz.ctl_err != nullptr && !p.hb && p.logits_dbg == nullptr &&
+      !p.fz.state_out)
+    return launch_ada_std<GP>(p, smem, grid, stream, pdl);
   switch (p.st.d) {
     case 128: return launch_ada_dk<GP, 128>(p, smem, grid, stream, pdl);
     case 64: return launch_ada_dk<GP, 64>(p, smem, grid, stream, pdl);
@@ -1690,6 +1695,7 @@ extern "C" int sphkv_ada_decode_fused(const sphkv_store_t* st, const float* q, i
   FusedCtl f;
   int rc = make_fused(f, slot_group, slot_begin, n_groups, ctl, out, dynamic);
   if (rc) return rc;
+  f.flag_units = 1;
   return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream);
 }
 
@@ -1722,6 +1728,7 @@ extern "C" int sphkv_ada_decode_live(const sphkv_store_t* st, const float* q, in
   f.top2 = top2;
   f.margins = margins;
   f.abs_rows = (flags & SPHKV_LIVE_ABS_ROWS) ? 1 : 0;
+  f.flag_units = 1;
   return ada_decode_impl(st, q, G, units, n_units, partials, nullptr, nullptr, grid, f, stream,
                          (flags & SPHKV_LIVE_AFTER_MUTATION) != 0);
 }

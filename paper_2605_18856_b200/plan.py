@@ -103,7 +103,8 @@ def _page_cost(rows, d):
 
 
 def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
-               dynamic=False, tail=0.0, tail_pieces=2, open_end=False) -> DecodePlan:
+               dynamic=False, tail=0.0, tail_pieces=2, open_end=False,
+               open_reserve_tiles=0.0) -> DecodePlan:
     """Plan a decode pass over `groups` (default: every group of the store).
 
     `tail` (with units_per_cta=1, implies dynamic): each CTA's share is cut
@@ -113,7 +114,12 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
 
     `ranges` (optional, one (begin, end) per group) restricts each group to a
     contiguous range of its pointer list -- the page-range split of one
-    sequence across ranks; see `plan_store_range`."""
+    sequence across ranks; see `plan_store_range`.
+
+    `open_end`: each group's last unit runs to the list's current end (decode
+    steps that append); with `open_reserve_tiles` (units_per_cta=1) that unit
+    is cut that many average tiles short of an equal share, leaving room for
+    the partly filled pages appends open (one per tier, each a whole tile)."""
     n, rows, plen, ptr = store._host()
     if groups is None:
         groups = np.arange(store.groups)
@@ -147,13 +153,18 @@ def plan_store(store, groups=None, grid=SM_COUNT, units_per_cta=2, ranges=None,
                 pieces.append([0, int(g), rb, rb])
                 continue
             c = np.cumsum(pbytes[lst])
+            # open-ended last unit: cut the list as if it carried
+            # open_reserve_tiles more (average) tiles, which the last unit owns
+            extra = 0.0
+            if open_end and open_reserve_tiles > 0:
+                extra = open_reserve_tiles * float(c[-1]) / max(int(ptiles[lst].sum()), 1)
             if tail > 0:
                 ns = int(n) * int(tail_pieces)
                 fr = [(1.0 - tail) * k / n for k in range(1, int(n) + 1)]
                 fr += [(1.0 - tail) + tail * j / ns for j in range(1, ns)]
             else:
                 fr = [k / n for k in range(1, int(n))]
-            cuts = [0] + [int(np.searchsorted(c, c[-1] * f, side="left")) + 1
+            cuts = [0] + [int(np.searchsorted(c, (c[-1] + extra) * f, side="left")) + 1
                           for f in fr] + [len(lst)]
             cuts = np.minimum(np.maximum.accumulate(cuts), len(lst))
             for s0, e0 in zip(cuts[:-1], cuts[1:]):

@@ -42,7 +42,7 @@ class DecodeStepper:
     the recent-segment weight).  gate_cfg: GateConfig or None (no gate)."""
 
     def __init__(self, store, G, u_hat, s_hat, r_q, *, lam=0.0, omega=1.0, alpha_theta=1.0,
-                 alpha_r=1.0, gate_cfg=None, per_layer=True, grid=148):
+                 alpha_r=1.0, gate_cfg=None, per_layer=True, grid=148, open_reserve_tiles=16.0):
         import torch
 
         self.l = _lib.require_gpu()
@@ -62,8 +62,10 @@ class DecodeStepper:
                      for l in range(L)]
         else:
             lists = [list(range(groups))]
-        self.plans = [plan_store(store, groups=g, grid=grid, units_per_cta=1, open_end=True)
-                      for g in lists]
+        # the last unit of a group also decodes the pages the steps append (a
+        # partly filled page per tier in use): it gets a few tiles less prefill
+        self.plans = [plan_store(store, groups=g, grid=grid, units_per_cta=1, open_end=True,
+                                 open_reserve_tiles=open_reserve_tiles) for g in lists]
         self.q = torch.zeros((groups, G, d), dtype=torch.float32, device=dev)
         self.k_new = torch.zeros((groups, d), dtype=torch.float32, device=dev)
         self.v_new = torch.zeros((groups, dv), dtype=torch.float16, device=dev)
@@ -159,12 +161,17 @@ class DecodeStepper:
 
     def finish(self):
         """Synchronize, surface append errors (pool / pointer-list capacity,
-        unknown tier) and refresh the store's host views and table placement."""
+        unknown tier) and decode units that outgrew the tile list, and refresh
+        the store's host views and table placement."""
         import torch
 
         torch.cuda.synchronize()
         err = int(self.err.item())
+        oversize = any(int(p.ctl[len(p.group_ids) + 2].item()) for p in self.plans)
         self.st._invalidate()
+        if oversize:
+            raise RuntimeError("a live decode unit outgrew the kernel's tile list "
+                               "(sphkv_unit_tile_cap); build a new DecodeStepper")
         if err == 3:
             raise RuntimeError("store pool exhausted during decode appends")
         if err == 4:
