@@ -15,7 +15,11 @@
 
 namespace sphkv {
 
+#ifdef SPHKV_MUFU12  // 12-bit tier on MUFU sin/cos: no table for it
+constexpr int LUT_MAX_BITS = 11;
+#else
 constexpr int LUT_MAX_BITS = 12;
+#endif
 #ifndef SPHKV_LUT_KB
 #define SPHKV_LUT_KB 124
 #endif

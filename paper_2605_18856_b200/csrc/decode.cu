@@ -52,6 +52,9 @@ constexpr int ADA_TI = TTI;        // items per tile (TK per lane)
 #define SPHKV_NS 12
 #endif
 constexpr int ADA_NS = SPHKV_NS;   // P slots
+// a logit warp waits for its slot by mbarrier PARITY: with NS or more warps
+// blocked on slots, a claim NS tiles ahead could pass on a stale phase
+static_assert(ADA_NS > ADA_NL, "more P slots than logit warps");
 #ifndef SPHKV_NV
 #define SPHKV_NV 2
 #endif
