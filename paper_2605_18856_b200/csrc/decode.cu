@@ -971,6 +971,9 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_std(const AdaPara
   if (u < p.n_units && warp == ADA_NL && lane == 0)
     for (int k = 0; k < *ntiles_s && k < ADA_NV; ++k) issue_v(k, 0u);
   ptx::griddep_wait();  // inputs below (q) may come from the previous grid
+#ifdef SPHKV_DBG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x] = gtimer();
+#endif
   __syncthreads();
   ptx::griddep_launch_dependents();
   bool lut_ready = false, first = true;
@@ -1097,6 +1100,9 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_std(const AdaPara
     u = p.fz.dynamic ? s_next : u + gridDim.x;
   }
   fused_kernel_exit(p.fz);
+#ifdef SPHKV_DBG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x + 1] = gtimer();
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -14,6 +14,8 @@ from __future__ import annotations
 
 import heapq
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -93,6 +95,9 @@ def _page_bytes(rows, tiers, d, d_v, P):
 PS_PER_ITEM = {1: 80, 2: 80, 3: 120, 4: 116, 5: 140, 6: 190, 7: 141, 8: 160, 9: 170, 10: 180,
                11: 190, 12: 195, 13: 400, 14: 430, 15: 470, 16: 500}
 PAGE_COST_PS = 200
+if os.environ.get("SPHKV_PS_PER_ITEM"):  # experiments: "2:80,4:116,..." overrides
+    PS_PER_ITEM.update({int(a): int(b) for a, b in
+                        (kv.split(":") for kv in os.environ["SPHKV_PS_PER_ITEM"].split(","))})
 
 
 def _page_cost(rows, d):

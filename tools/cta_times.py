@@ -7,16 +7,19 @@ import bench
 import paper_2605_18856_b200 as sk
 from paper_2605_18856_b200 import _lib, plan as planmod
 
-W = bench.build_workload("c5")
-st, wl = W["st"], W["wl"]
+W = bench.build_workload("c5", dense=False, parity=False)
+st, qall = W["st"], W["q"]
 B, L, H, G, T, d, _ = bench.CONFIGS["c5"]
 lib = _lib.lib()
-for l in (0, 5):
+import os
+LAYERS = [int(x) for x in os.environ.get("CTA_LAYERS", "0,5").split(",")]
+raw = {}
+for l in LAYERS:
     groups = [(b * L + l) * H + h for b in range(B) for h in range(H)]
     p = planmod.plan_store(st, groups=groups, units_per_cta=1)
     out = torch.empty((len(groups) * G, d), dtype=torch.float32, device="cuda")
     for _ in range(3):
-        sk.ada_decode(st, wl.queries, p, out=out)
+        sk.ada_decode(st, qall, p, out=out)
     torch.cuda.synchronize()
     buf = (ctypes.c_ulonglong * (2 * p.grid))()
     lib.sphkv_debug_cta_times.argtypes = [ctypes.c_void_p, ctypes.c_int]
@@ -51,3 +54,9 @@ for l in (0, 5):
     for i in np.argsort(dur)[:3]:
         print("   fast cta", i, "dur %.1f" % dur[i], "pred %.1f" % (pc[i] / 1e6), "items by bits",
               {b: int(ab[i][b]) for b in range(16) if ab[i][b]})
+    raw[f"dur{l}"] = dur
+    raw[f"ab{l}"] = ab
+    raw[f"pc{l}"] = pc
+    raw[f"np{l}"] = np.array([b - a for a, b in zip(u["ptr_begin"], u["ptr_end"])])
+if os.environ.get("CTA_OUT"):
+    np.savez(os.environ["CTA_OUT"], **raw)
