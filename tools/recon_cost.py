@@ -10,8 +10,8 @@ import bench
 import paper_2605_18856_b200 as sk
 from paper_2605_18856_b200 import _lib, plan as planmod
 
-W = bench.build_workload("c5")
-st, wl = W["st"], W["wl"]
+W = bench.build_workload("c5", dense=False, parity=False)
+st, qall = W["st"], W["q"]
 B, L, H, G, T, d, _ = bench.CONFIGS["c5"]
 groups = [(b * L + 0) * H + h for b in range(B) for h in range(H)]
 n, rows, plen, ptr = st._host()
@@ -22,19 +22,21 @@ items = int(counts.sum())
 stage = torch.empty((items, d), dtype=torch.float16, device="cuda")
 pid_t, off_t = torch.as_tensor(pids, device="cuda"), torch.as_tensor(off, device="cuda")
 lib = _lib.lib()
-gi = np.repeat(np.arange(len(groups)), [int(rows["count"][ptr[g, : plen[g]]].sum()) for g in groups])
-qh = wl.queries[groups].half()  # [groups, G, d]
-bounds = np.concatenate([[0], np.cumsum(np.bincount(gi, minlength=len(groups)))])
+per_group = [int(rows["count"][ptr[g, : plen[g]]].sum()) for g in groups]
+bounds = np.concatenate([[0], np.cumsum(per_group)]).astype(np.int64)
+dot_out = torch.empty((items, G), dtype=torch.float32, device="cuda")
 
 
-def recon():
+def recon():  # staging write: every item's key decoded to fp16 rows (sphkv_recon_keys)
     _lib.check(lib.sphkv_recon_keys(st.cptr, pid_t.data_ptr(), off_t.data_ptr(), len(pids),
                                     stage.data_ptr(), _lib.F16, _lib.stream_ptr()))
 
 
-def reread():
-    for k in range(len(groups)):
-        torch.matmul(stage[bounds[k]:bounds[k + 1]], qh[k].T)
+def reread():  # the dot's re-read of the staged rows, G query heads (sphkv_recon_dot)
+    for k, g in enumerate(groups):
+        a, b = int(bounds[k]), int(bounds[k + 1])
+        _lib.check(lib.sphkv_recon_dot(stage[a:b].data_ptr(), _lib.F16, b - a, d, qall[g].data_ptr(),
+                                       G, dot_out[a:b].data_ptr(), _lib.stream_ptr()))
 
 
 def timeit(fn, it=10):
@@ -52,7 +54,7 @@ def timeit(fn, it=10):
 
 p = planmod.plan_store(st, groups=groups, units_per_cta=1)
 out = torch.empty((len(groups) * G, d), dtype=torch.float32, device="cuda")
-t_ada = timeit(lambda: sk.ada_decode(st, wl.queries, p, out=out))
+t_ada = timeit(lambda: sk.ada_decode(st, qall, p, out=out))
 t_w = timeit(recon)
 t_r = timeit(reread)
 tax = items * d * 2
