@@ -26,6 +26,7 @@
 //   The CTA finishing a group's last split merges the group's partials
 //   (fused LSE merge) into output rows, a partial state (page-range split),
 //   and the gate margins when asked.
+#include <cstdlib>
 #include "common.cuh"
 #include "ptx.cuh"
 #include "ada_tile.cuh"
@@ -112,6 +113,10 @@ struct AdaParams {
   int hb;                   // 2-bit tier decodes through the h-byte tables
   int pslot_bytes, prow_bytes, prows;  // P slot: prows rows of TI fp16 weights + header
   FusedCtl fz;
+  // pipelined unit transitions (k_ada_decode_pipe): second q / tile-list
+  // buffers and the unit-info ring
+  uint32_t smem_q2, smem_tiles2, smem_info;
+  int pipe;
 };
 
 __device__ __forceinline__ int tier_index(const sphkv_store_t& st, int tier_id) {
@@ -830,7 +835,8 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode(const AdaParams p
 // tile count (also in smem); a unit with more tiles than the list holds is
 // flagged in ctl_err (the launch's units are unusable: SPHKV_E_CAPACITY).
 __device__ int build_tiles_std(const sphkv_store_t& st, const sphkv_unit_t& u, int TI,
-                               TileEntry* tiles, int* ntiles_smem, int lane, int32_t* ctl_err) {
+                               TileEntry* tiles, int* ntiles_smem, int lane, int32_t* ctl_err,
+                               int cap = MAX_UNIT_TILES) {
   const int* ptr = st.ptr + (size_t)u.group * st.ptr_cap;
   const int pe = unit_end(st, u);  // open-ended (live) units: the list's current end
   int nt = 0, items = 0;
@@ -851,7 +857,7 @@ __device__ int build_tiles_std(const sphkv_store_t& st, const sphkv_unit_t& u, i
     }
     int t0 = nt + ts - t, i0 = items + is - cnt;
     for (int s = 0; s < t; ++s) {
-      if (t0 + s < MAX_UNIT_TILES) {
+      if (t0 + s < cap) {
         tiles[t0 + s].page = pid;
         tiles[t0 + s].sub_off = (s << 24) | (i0 + s * TI);
       }
@@ -860,8 +866,8 @@ __device__ int build_tiles_std(const sphkv_store_t& st, const sphkv_unit_t& u, i
     items += __shfl_sync(0xffffffffu, is, 31);
   }
   if (lane == 0) {
-    *ntiles_smem = nt < MAX_UNIT_TILES ? nt : MAX_UNIT_TILES;
-    if (nt > MAX_UNIT_TILES && ctl_err != nullptr) atomicExch(ctl_err, SPHKV_E_CAPACITY);
+    *ntiles_smem = nt < cap ? nt : cap;
+    if (nt > cap && ctl_err != nullptr) atomicExch(ctl_err, SPHKV_E_CAPACITY);
   }
   return nt;
 }
@@ -1100,6 +1106,369 @@ __global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_std(const AdaPara
     u = p.fz.dynamic ? s_next : u + gridDim.x;
   }
   fused_kernel_exit(p.fz);
+#ifdef SPHKV_DBG_TIMING
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x + 1] = gtimer();
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined unit transitions (opt-in, SPHKV_PIPE=1): the standard body's
+// per-unit drain (every warp waits at a block barrier for the slowest logit
+// warp's last tile and the PV warp's tail, then the next tile list, q rows,
+// prefetches and V copies start cold) made dynamic pieces cost 18-40 us per
+// launch (profiles/r2/occupancy).  Here the units of a CTA form one continuous
+// tile sequence: logit warps claim from one counter across units and move
+// into the next unit without a barrier; the PV warp consumes in order, writes
+// each unit's partial, does the group's merge count (and the merge, when
+// last) alone, then builds the tile list and q rows of the unit after next
+// into the buffers the finished unit frees (double-buffered), and keeps the
+// V ring running across the boundary.
+// ---------------------------------------------------------------------------
+constexpr int PIPE_MAXU = 64;   // units per CTA (unit-info ring; never wraps)
+constexpr int PIPE_TILES = 256; // tile-list capacity per buffer (a longer unit is flagged)
+
+// Block-wide merge of group gi's splits into its output rows (the merge half
+// of fused_unit_done; the count was won earlier).  All threads call it.
+__device__ __noinline__ void merge_group_block(const int32_t* slot_begin, int32_t* ctl, float* out,
+                                               const float* partials, int gi, int G, int d_v,
+                                               float* s_ml) {
+  __threadfence();
+  const int b = slot_begin[gi], e = slot_begin[gi + 1];
+  const int64_t stride = (int64_t)G * (d_v + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int g = warp; g < G; g += nw) {
+    float M = -INFINITY;
+    for (int s = b + lane; s < e; s += 32) M = fmaxf(M, __ldcg(partials + s * stride + g));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float L = 0.f;
+    for (int s = b + lane; s < e; s += 32) {
+      const float m = __ldcg(partials + s * stride + g);
+      const float l = __ldcg(partials + s * stride + G + g);
+      L += (m != -INFINITY) ? l * exp2f(m - M) : 0.f;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+    if (lane == 0) {
+      s_ml[g] = M;
+      s_ml[8 + g] = L;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * d_v; i += blockDim.x) {
+    const int g = i / d_v, j = i % d_v;
+    const float M = s_ml[g], L = s_ml[8 + g];
+    float a = 0.f;
+#pragma unroll 8
+    for (int s = b; s < e; ++s) {
+      const float m = __ldcg(partials + s * stride + g);
+      const float v = __ldcg(partials + s * stride + 2 * G + (int64_t)g * d_v + j);
+      a += (m != -INFINITY) ? v * exp2f(m - M) : 0.f;
+    }
+    out[((int64_t)gi * G + g) * d_v + j] = (L > 0.f) ? a / L : 0.f;
+  }
+  if (threadIdx.x == 0) ctl[gi] = 0;  // every split of gi has counted: re-arm
+  __syncthreads();
+}
+
+template <int GP>
+__global__ void __launch_bounds__(ADA_THREADS, 1) k_ada_decode_pipe(const AdaParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const sphkv_store_t& st = p.st;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  TileEntry* tl0 = reinterpret_cast<TileEntry*>(smem + p.smem_tiles);
+  TileEntry* tl1 = reinterpret_cast<TileEntry*>(smem + p.smem_tiles2);
+  int4* info = reinterpret_cast<int4*>(smem + p.smem_info);  // {base, nt (<0: end), unit, 0}
+  int* ctr = reinterpret_cast<int*>(info + PIPE_MAXU);       // [0] tile claims, [1] units built,
+                                                             // [2] deferred merges
+  int* mlist = ctr + 4;                                      // [PIPE_MAXU] groups to merge
+  uint8_t* pslots = smem + p.smem_p;
+  uint8_t* vslots = smem + p.smem_v;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.smem_bar);
+  uint64_t* p_full = bars;
+  uint64_t* p_empty = bars + ADA_NS;
+  uint64_t* v_full = bars + 2 * ADA_NS;
+  uint64_t* v_empty = bars + 2 * ADA_NS + ADA_NV;
+  uint64_t* lut_bar = bars + 2 * ADA_NS + 2 * ADA_NV;
+  const int d = st.d, P = st.page_size, TI = p.TI, dvp = p.dvp, MT = dvp / 16;
+  const uint32_t vbytes = (uint32_t)TI * dvp * 2;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ADA_NS; ++i) {
+      ptx::mbar_init(&p_full[i], 1);
+      ptx::mbar_init(&p_empty[i], ADA_NPV);
+    }
+    for (int i = 0; i < ADA_NV; ++i) {
+      ptx::mbar_init(&v_full[i], 1);
+      ptx::mbar_init(&v_empty[i], ADA_NPV);
+    }
+    ptx::mbar_init(lut_bar, 1);
+    ptx::fence_mbar_init();
+    if (p.lut_global != nullptr && p.lut_bytes > 0) {
+      ptx::mbar_arrive_expect_tx(lut_bar, (uint32_t)p.lut_bytes);
+      ptx::bulk_g2s(smem, p.lut_global, (uint32_t)p.lut_bytes, lut_bar);
+    } else {
+      ptx::mbar_arrive(lut_bar);
+    }
+    ctr[0] = 0;
+    ctr[1] = 0;
+    ctr[2] = 0;
+  }
+  if (p.lut_global == nullptr) lut_fill(smem, st.tiers, st.n_tiers, p.lut_off, threadIdx.x, blockDim.x);
+  auto prefetch_tile = [&](const TileEntry* tl, int t, int nt) {
+    if (t < nt) {
+      const TileEntry tn = tl[t];
+      const int sb = tn.sub_off >> 24;
+      const sphkv_page_t pn = st.pages[tn.page];
+      const uint64_t W4 = (uint64_t)item_words(d, pn.abits) * 128;
+      const int g0 = sb * TI / 32, ng = (TI + 31) / 32;
+      ptx::bulk_prefetch_l2(st.codes + pn.code_off + g0 * W4, (uint32_t)(ng * W4));
+      if (sb == 0) {
+        const uint64_t ab = angle_part_bytes(d, P, pn.abits);
+        ptx::bulk_prefetch_l2(st.codes + pn.code_off + ab,
+                              (uint32_t)(code_block_bytes(d, P, pn.abits, pn.rbits) - ab));
+      }
+    }
+  };
+  const float qscale = kLog2e * rsqrtf((float)d);
+  __syncthreads();  // barriers + counters initialised
+
+  if (warp < ADA_NL) {
+    // ---------------- logit warps ----------------
+    ptx::griddep_wait();
+    ptx::griddep_launch_dependents();
+    ptx::mbar_wait(lut_bar, 0);
+    int j = -1, ubase = 0, unt = 0;
+    const TileEntry* tl = tl0;
+    uint32_t qoff = p.smem_q;
+    for (;;) {
+      int k = 0;
+      if (lane == 0) k = atomicAdd(&ctr[0], 1);
+      k = __shfl_sync(0xffffffffu, k, 0);
+      bool end = false;
+      while (j < 0 || k >= ubase + unt) {  // move to the unit holding tile k
+        ++j;
+        if (lane == 0)
+          while (*reinterpret_cast<volatile int*>(&ctr[1]) <= j) __nanosleep(64);
+        __syncwarp();
+        __threadfence_block();
+        const volatile int4* vin = &info[j];
+        const int4 in = make_int4(vin->x, vin->y, vin->z, vin->w);
+        if (in.y < 0) {
+          end = true;
+          break;
+        }
+        ubase = in.x;
+        unt = in.y;
+        tl = (j & 1) ? tl1 : tl0;
+        qoff = (j & 1) ? p.smem_q2 : p.smem_q;
+      }
+      if (end) break;
+      const int kl = k - ubase;
+      if (lane == 0) prefetch_tile(tl, kl + SPHKV_PF_DIST, unt);
+      const TileEntry te = tl[kl];
+      const int sub = te.sub_off >> 24;
+      const sphkv_page_t pg = st.pages[te.page];
+      const int ti = tier_index(st, pg.tier);
+      float lg[TK][2 * GP];
+      ada_logit_dispatch<GP, -1>(pg.abits, st.codes, d, P, pg, sub, lane, smem, qoff,
+                                 p.lut_off[ti], lg);
+      uint32_t valid = 0;
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        const int it = sub * TI + 32 * kk + lane;
+        if (32 * kk + lane < TI && it < pg.count) valid |= 1u << kk;
+      }
+      const uint32_t gk = (uint32_t)k;
+      const int ps = gk % ADA_NS;
+      ptx::mbar_wait(&p_empty[ps], ((gk / ADA_NS) & 1) ^ 1);
+      write_pslot<2 * GP>(pslots + ps * p.pslot_bytes, p.prow_bytes, p.prows, TI, lane, p.G, lg,
+                          valid, false);
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&p_full[ps]);
+    }
+  } else {
+    // ---------------- PV warp: consumer, unit builder, V producer ----------------
+    const uint64_t vpol = ptx::policy_evict_first();
+    int nbuilt = 0, tiles_built = 0;  // units built, tiles of the built units
+    int last_unit = -1;               // unit id of the last unit built (static stepping)
+    bool ended = false;
+    // build local unit `jj` (ordinal) = unit id `u` (< 0: end) into buffer jj & 1
+    auto build = [&](int u, bool load_q) {
+      const int jj = nbuilt;
+      if (u < 0 || u >= p.n_units || jj >= PIPE_MAXU - 1) {
+        if (lane == 0) info[jj] = make_int4(tiles_built, -1, -1, 0);
+        ended = true;
+      } else {
+        TileEntry* tl = (jj & 1) ? tl1 : tl0;
+        int* nts = reinterpret_cast<int*>(tl + PIPE_TILES);
+        int nt = build_tiles_std(st, p.units[u], TI, tl, nts, lane, p.fz.ctl_err, PIPE_TILES);
+        nt = nt < PIPE_TILES ? nt : PIPE_TILES;
+        if (load_q) {
+          float2* qs = reinterpret_cast<float2*>(smem + ((jj & 1) ? p.smem_q2 : p.smem_q));
+          const float* qg = p.q + (size_t)p.units[u].group * p.G * d;
+          for (int i = lane; i < d * GP; i += 32) {
+            const int jr = i / GP, g2 = i % GP;
+            const float a = (2 * g2 < p.G) ? qg[(size_t)(2 * g2) * d + jr] * qscale : 0.f;
+            const float b = (2 * g2 + 1 < p.G) ? qg[(size_t)(2 * g2 + 1) * d + jr] * qscale : 0.f;
+            qs[jr * (q_row_bytes(GP) / 8) + g2] = make_float2(a, b);
+          }
+        }
+        __syncwarp();
+        if (lane < SPHKV_PF_DIST) prefetch_tile(tl, lane, nt);
+        if (lane == 0) info[jj] = make_int4(tiles_built, nt, u, 0);
+        tiles_built += nt;
+        last_unit = u;
+      }
+      __syncwarp();
+      __threadfence_block();
+      if (lane == 0) *reinterpret_cast<volatile int*>(&ctr[1]) = jj + 1;
+      ++nbuilt;
+    };
+    auto next_unit = [&]() -> int {
+      if (ended) return -1;
+      int u = 0;
+      if (p.fz.dynamic) {
+        if (lane == 0) u = atomicAdd(&p.fz.ctl[p.fz.n_groups], 1) + (int)gridDim.x;
+        u = __shfl_sync(0xffffffffu, u, 0);
+      } else {
+        u = last_unit + (int)gridDim.x;
+      }
+      return u;
+    };
+    // V copy of sequence number s (its unit is built: s < tiles_built); the
+    // unit cursor (vj, vb, ve) only moves forward (lane 0's registers)
+    int vj = 0, vb = 0, ve = 0;
+    auto issue_v = [&](uint32_t s) {
+      while ((int)s >= ve) {
+        const int4 in = info[++vj];
+        vb = in.x;
+        ve = in.x + (in.y > 0 ? in.y : 0);
+      }
+      const TileEntry* tl = (vj & 1) ? tl1 : tl0;
+      const TileEntry te = tl[s - vb];
+      const int sub = te.sub_off >> 24;
+      const int vs = s % ADA_NV;
+      ptx::mbar_wait(&v_empty[vs], ((s / ADA_NV) & 1) ^ 1);
+      const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)sub * TI) * dvp;
+      ptx::fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
+      ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
+    };
+    uint32_t v_next = 0;
+    // prologue: unit 0 (static: blockIdx.x) tile list + V copies before the
+    // wait; its q rows, the second unit and the claims after it
+    {
+      const int u0 = (int)blockIdx.x;
+      if (u0 < p.n_units) {
+        TileEntry* tl = tl0;
+        int* nts = reinterpret_cast<int*>(tl + PIPE_TILES);
+        int nt = build_tiles_std(st, p.units[u0], TI, tl, nts, lane, p.fz.ctl_err, PIPE_TILES);
+        nt = nt < PIPE_TILES ? nt : PIPE_TILES;
+        __syncwarp();
+        if (lane < SPHKV_PF_DIST) prefetch_tile(tl, lane, nt);
+        if (lane == 0) {
+          info[0] = make_int4(0, nt, u0, 0);
+          for (; v_next < (uint32_t)nt && v_next < (uint32_t)ADA_NV; ++v_next) {
+            const TileEntry te = tl[v_next];
+            const int vs = v_next % ADA_NV;
+            const uint16_t* src = st.values + ((size_t)te.page * P + (size_t)(te.sub_off >> 24) * TI) * dvp;
+            ptx::mbar_arrive_expect_tx(&v_full[vs], vbytes);
+            ptx::bulk_g2s_hint(vslots + (size_t)vs * vbytes, src, vbytes, &v_full[vs], vpol);
+          }
+        }
+        tiles_built = nt;
+        last_unit = u0;
+        ve = nt;
+      }
+      ptx::griddep_wait();
+#ifdef SPHKV_DBG_TIMING
+      if (lane == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x] = gtimer();
+#endif
+      if (u0 < p.n_units) {
+        float2* qs = reinterpret_cast<float2*>(smem + p.smem_q);
+        const float* qg = p.q + (size_t)p.units[u0].group * p.G * d;
+        for (int i = lane; i < d * GP; i += 32) {
+          const int jr = i / GP, g2 = i % GP;
+          const float a = (2 * g2 < p.G) ? qg[(size_t)(2 * g2) * d + jr] * qscale : 0.f;
+          const float b = (2 * g2 + 1 < p.G) ? qg[(size_t)(2 * g2 + 1) * d + jr] * qscale : 0.f;
+          qs[jr * (q_row_bytes(GP) / 8) + g2] = make_float2(a, b);
+        }
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) *reinterpret_cast<volatile int*>(&ctr[1]) = 1;
+        nbuilt = 1;
+        build(next_unit(), true);
+      } else {
+        build(-1, false);
+      }
+    }
+    ptx::griddep_launch_dependents();
+    PVState<ADA_MTW> s;
+    const bool fast_pv = (dvp == 128 && TI == ADA_TI && MT == ADA_MTW);
+    const bool fast64 = (dvp == 64 && TI == ADA_TI);
+    for (int j = 0;; ++j) {
+      const int4 in = info[j];
+      if (in.y < 0) break;
+      pv_init(s);
+      for (int k = 0; k < in.y; ++k) {
+        const uint32_t gk = (uint32_t)(in.x + k);
+        const int vs = gk % ADA_NV, ps = gk % ADA_NS;
+        ptx::mbar_wait(&v_full[vs], (gk / ADA_NV) & 1);
+        ptx::mbar_wait(&p_full[ps], (gk / ADA_NS) & 1);
+        if (fast_pv)
+          pv_tile_128<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                               p.prow_bytes, p.prows, 0, p.G, lane, false);
+        else if (fast64)
+          pv_tile_128<ADA_MTW, ADA_TI / 16, 64, 4>(s, pslots + ps * p.pslot_bytes,
+                                                   vslots + (size_t)vs * vbytes, p.prow_bytes,
+                                                   p.prows, 0, p.G, lane, false);
+        else
+          pv_tile<ADA_MTW>(s, pslots + ps * p.pslot_bytes, vslots + (size_t)vs * vbytes,
+                           p.prow_bytes, p.prows, TI, dvp, 0, MT, p.G, lane, false);
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&p_empty[ps]);
+          ptx::mbar_arrive(&v_empty[vs]);
+          for (; v_next < gk + 1 + ADA_NV && v_next < (uint32_t)tiles_built; ++v_next) issue_v(v_next);
+        }
+        __syncwarp();
+      }
+      const sphkv_unit_t unit = p.units[in.z];
+      float* part = p.partials + (size_t)unit.out_slot * ((size_t)p.G * (st.d_v + 2));
+      pv_write<ADA_MTW>(s, part, p.G, st.d_v, 0, MT, true, lane, nullptr);
+      // merge count; the last split of a group defers the (block-wide) merge
+      // to the CTA's end
+      if (p.fz.slot_group != nullptr) {
+        __threadfence();
+        __syncwarp();
+        const int gi = p.fz.slot_group[unit.out_slot];
+        if (lane == 0 && gi >= 0) {
+          const int ns = p.fz.slot_begin[gi + 1] - p.fz.slot_begin[gi];
+          if (atomicAdd(&p.fz.ctl[gi], 1) == ns - 1) mlist[ctr[2]++] = gi;
+        }
+      }
+      // the buffers of unit j are free: build unit j + 2
+      if (!ended) build(next_unit(), true);
+      if (lane == 0)
+        for (; v_next < (uint32_t)(in.x + in.y) + ADA_NV && v_next < (uint32_t)tiles_built; ++v_next)
+          issue_v(v_next);
+      __syncwarp();
+    }
+    if (p.fz.dynamic && lane == 0) {
+      __threadfence();
+      if (atomicAdd(&p.fz.ctl[p.fz.n_groups + 1], 1) == (int)gridDim.x - 1) {
+        p.fz.ctl[p.fz.n_groups] = 0;
+        p.fz.ctl[p.fz.n_groups + 1] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  {
+    float* s_ml = reinterpret_cast<float*>(bars + 2 * ADA_NS + 2 * ADA_NV + 2);
+    const int nm = ctr[2];
+    for (int i = 0; i < nm; ++i)
+      merge_group_block(p.fz.slot_begin, p.fz.ctl, p.fz.out, p.partials, mlist[i], p.G, st.d_v, s_ml);
+  }
 #ifdef SPHKV_DBG_TIMING
   if (threadIdx.x == 0 && blockIdx.x < 1024) g_cta_t[2 * blockIdx.x + 1] = gtimer();
 #endif
@@ -1522,7 +1891,15 @@ static int launch_ada_std(AdaParams& p, size_t smem, int grid, cudaStream_t stre
 }
 
 template <int GP>
+static int launch_ada_pipe(AdaParams& p, size_t smem, int grid, cudaStream_t stream, bool pdl) {
+  auto kern = k_ada_decode_pipe<GP>;
+  SPHKV_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return launch_pdl(kern, p, grid, ADA_THREADS, smem, stream, pdl);
+}
+
+template <int GP>
 static int launch_ada(AdaParams& p, size_t smem, int grid, cudaStream_t stream, bool pdl) {
+  if (p.pipe) return launch_ada_pipe<GP>(p, smem, grid, stream, pdl);
   // the fused path (outputs, gate margins, absolute rows, live units) runs the
   // round-1 kernel body (see k_ada_decode_std); state output, debug logits
   // and the h-byte tables take the general kernel
@@ -1586,6 +1963,23 @@ static int ada_decode_impl(const sphkv_store_t* st, const float* q, int G,
   off = align_up(off + (size_t)st->d * q_row_bytes(GP), 128);
   p.smem_tiles = (uint32_t)off;
   off = align_up(off + MAX_UNIT_TILES * sizeof(TileEntry) + 16, 128);
+  // pipelined unit transitions (experiment, SPHKV_PIPE=1): plain fused
+  // outputs only (no margins / state / live / debug logits / h-byte tables)
+  {
+    const char* e = getenv("SPHKV_PIPE");
+    p.pipe = (e != nullptr && e[0] == '1' && ADA_NPV == 1 && fz.flag_units && fz.ctl_err != nullptr && !p.hb &&
+              logits_dbg == nullptr && !fz.state_out && fz.margins == nullptr &&
+              fz.slot_group != nullptr && !fz.abs_rows && !live) ? 1 : 0;
+  }
+  if (p.pipe) {  // two PIPE_TILES lists (+ count word each) inside the tile-list region
+    static_assert(2 * (PIPE_TILES * sizeof(TileEntry) + 16) <= MAX_UNIT_TILES * sizeof(TileEntry) + 16 + 128,
+                  "pipe tile lists fit the standard tile-list region");
+    p.smem_tiles2 = p.smem_tiles + (uint32_t)align_up(PIPE_TILES * sizeof(TileEntry) + 16, 16);
+    p.smem_info = (uint32_t)off;
+    off = align_up(off + PIPE_MAXU * 16 + 16 + PIPE_MAXU * 4, 128);
+    p.smem_q2 = (uint32_t)off;
+    off = align_up(off + (size_t)st->d * q_row_bytes(GP), 128);
+  }
   p.prow_bytes = p.TI * 2 + PROW_PAD;
   p.prows = G <= 4 ? 4 : 8;
   p.pslot_bytes = (int)align_up(p.prows * p.prow_bytes + 96, 16);  // hdr: m, sum, top-2

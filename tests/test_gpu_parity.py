@@ -410,6 +410,31 @@ def test_dynamic_plan_back_to_back(sk):
     assert int(dyn.ctl.abs().sum()) == 0
 
 
+@pytest.mark.parametrize("kw", [dict(grid=148, units_per_cta=1),
+                                dict(grid=40, units_per_cta=1, tail=0.3, tail_pieces=3),
+                                dict(grid=40, units_per_cta=4, dynamic=True)])
+def test_pipelined_unit_transitions_match_standard(sk, kw, monkeypatch):
+    """k_ada_decode_pipe (SPHKV_PIPE=1: one continuous tile sequence across a
+    CTA's units, merges deferred to the CTA's end) gives the standard kernel
+    body's outputs bit for bit, back to back under PDL, and re-arms every
+    control word."""
+    import torch
+
+    st, wl = _mixed_store(sk, 60000, seed=6)
+    plan = sk.plan_store(st, **kw)
+    monkeypatch.setenv("SPHKV_PIPE", "0")
+    ref = sk.ada_decode(st, wl.queries, plan)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("SPHKV_PIPE", "1")
+    outs = [torch.empty_like(ref) for _ in range(4)]
+    for o in outs:
+        sk.ada_decode(st, wl.queries, plan, out=o)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(ref, o)
+    assert int(plan.ctl.abs().sum()) == 0
+
+
 @pytest.mark.parametrize("world", [2, 3, 8])
 def test_page_range_split_two_level_merge(sk, world):
     """Multi-GPU data path on one device: each simulated rank decodes its
